@@ -1,0 +1,114 @@
+/*
+ * libzpp.so - C ABI of the B200-native ZeroPP engine.
+ *
+ * The reference (arxiv 2402.03791, package `zeroppsim`) is a CPU simulator whose
+ * executor slot is `simulate(sched, model, cfg, placement, costs)`
+ * (pkg/src/zeroppsim/simulation.py:90-158): every task's work is a cost number
+ * (`_duration`, simulation.py:80-87; task payloads schedules.py:28-91).  The
+ * functions below are the real-hardware operators behind those task records;
+ * the Python host (paper_2402_03791_b200/engine) binds them with ctypes, as a
+ * reference maintainer would.
+ *
+ * Conventions: plain pointers (device memory unless noted), int64 sizes,
+ * `stream` is a cudaStream_t passed as uintptr_t, no allocation inside (caller
+ * passes workspaces), return 0 on success or a ZPP_ERR_* / CUDA / NCCL code with
+ * zpp_last_error() describing it.  Kernels are re-entrant per stream; calls on one
+ * communicator must be serialised by the caller (NCCL rule).
+ */
+#ifndef ZPP_H
+#define ZPP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZPP_OK 0
+#define ZPP_ERR_ARG 1001
+#define ZPP_ERR_CUDA 1002
+#define ZPP_ERR_NCCL 1003
+#define ZPP_ERR_DRIVER 1004
+
+/* GEMM epilogues (low 4 bits of `epilogue`) */
+#define ZPP_EPI_BF16 0       /* C = acc (+bias[n]) (+resid[m,n])                        */
+#define ZPP_EPI_BF16_GELU 1  /* aux = acc+bias (pre-activation, optional), C = gelu(aux) (+resid) */
+#define ZPP_EPI_BF16_DGELU 2 /* C = acc * gelu'(aux[m,n])   (fc2 dgrad fused with GeLU bwd) */
+#define ZPP_EPI_F32 3        /* C(f32) = acc                                              */
+#define ZPP_EPI_F32_ACC 4    /* C(f32) += acc   (wgrad accumulation into the stage grad)   */
+
+const char* zpp_last_error(void);
+int zpp_num_sms(void);
+int zpp_version(void);
+
+/* ---- dense contractions (tcgen05 / TMEM / TMA) -------------------------------
+ * Replaces the cost of F/B/W tasks (schedules.py:51-66).
+ * C[M,N] (op)= sum_k A(m,k) B(n,k); A is K-major (A[m*lda+k]) or M-major
+ * (A[k*lda+m]); B is K-major (B[n*ldb+k]) or N-major (B[k*ldb+n]). bf16 in.     */
+int zpp_gemm(const void* A, int a_mn_major, long long lda, const void* B, int b_mn_major, long long ldb,
+             void* C, long long ldc, int M, int N, int K, int epilogue, const void* bias, const void* resid,
+             long long ldr, void* aux, long long ldaux, uintptr_t stream);
+
+/* ---- causal multi-head attention, qkv packed [b, s, 3, heads, d] bf16 --------- */
+int zpp_attn_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, int head_dim,
+                 uintptr_t stream);
+/* workspace: batch*heads*seq floats (row-wise dO.O) + batch*seq*heads*head_dim floats (dQ accum) */
+int zpp_attn_bwd(const void* qkv, const void* out, const float* lse, const void* dout, void* dqkv,
+                 float* workspace, int batch, int seq, int heads, int head_dim, uintptr_t stream);
+long long zpp_attn_bwd_workspace_floats(int batch, int seq, int heads, int head_dim);
+
+/* ---- LayerNorm (fp32 statistics) ---------------------------------------------- */
+int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
+                      int rows, int cols, float eps, uintptr_t stream);
+/* dx = LNbwd(dy) (+ dresid); dgamma/dbeta (fp32) += column sums. workspace: 2*cols*ceil(rows/64) floats */
+int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const void* gamma,
+                      const void* dresid, void* dx, float* dgamma, float* dbeta, float* workspace, int rows,
+                      int cols, uintptr_t stream);
+long long zpp_layernorm_bwd_workspace_floats(int rows, int cols);
+
+/* ---- bias gradient: dbias(f32)[c] += sum_r dy[r,c]; workspace cols*ceil(rows/64) floats */
+int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
+                   uintptr_t stream);
+
+/* ---- elementwise -------------------------------------------------------------- */
+int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream);
+
+/* ---- token + position embedding (stage 0) ------------------------------------ */
+int zpp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* out, int tokens, int seq,
+                  int hidden, uintptr_t stream);
+int zpp_embed_bwd(const int64_t* ids, const void* dout, float* dwte, float* dwpe, int tokens, int seq, int hidden,
+                  uintptr_t stream);
+
+/* ---- fused softmax cross-entropy (last stage): logits -> dlogits in place ----- */
+/* loss_sum(f32) += sum_r CE_r ; dlogits = (softmax - onehot) * grad_scale            */
+int zpp_xent_fwd_bwd(void* logits, long long ld, const int64_t* labels, float* loss_sum, int rows, int vocab,
+                     float grad_scale, uintptr_t stream);
+
+/* ---- ZeRO gradient path (RS_GRAD, schedules.py:76-78) --------------------------- */
+int zpp_cast_scale_f32_bf16(const float* in, void* out, long long n, float scale, uintptr_t stream);
+int zpp_accum_bf16_f32(const void* in, float* acc, long long n, uintptr_t stream);
+
+/* ---- sharded AdamW (OPT, schedules.py:89-91) ----------------------------------- */
+int zpp_adamw(float* master, float* exp_avg, float* exp_avg_sq, const float* grad, void* param_bf16, long long n,
+              float lr, float beta1, float beta2, float eps, float weight_decay, int step, uintptr_t stream);
+
+/* ---- deterministic parameter init: counter-hash Irwin-Hall(4) normal ---------- */
+/* value_i = mean + std * sqrt(3) * (u0+u1+u2+u3-2)  with u_j from splitmix64(seed, offset+i, j) */
+int zpp_init_param(float* master, void* param_bf16, long long n, unsigned long long seed, long long offset,
+                   float mean, float std, uintptr_t stream);
+
+/* ---- NCCL (AG_PARAM / RS_GRAD inside a ZeRO group, PP send/recv) ---------------- */
+int zpp_nccl_load(const char* libnccl_path);
+int zpp_nccl_unique_id(char* out128);
+int zpp_comm_init(const char* uid128, int nranks, int rank, void** comm);
+int zpp_comm_destroy(void* comm);
+/* dtype: 0 = bf16, 1 = f32 */
+int zpp_allgather(void* comm, const void* send, void* recv, long long count_per_rank, int dtype, uintptr_t stream);
+int zpp_reduce_scatter(void* comm, const void* send, void* recv, long long count_per_rank, int dtype,
+                       uintptr_t stream);
+int zpp_send(void* comm, const void* buf, long long count, int dtype, int peer, uintptr_t stream);
+int zpp_recv(void* comm, void* buf, long long count, int dtype, int peer, uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZPP_H */

@@ -1,0 +1,498 @@
+// HBM-bound kernels of the ZeroPP step: LayerNorm fwd/bwd, bias-grad column sums,
+// GeLU, embedding fwd/bwd, fused softmax cross-entropy, ZeRO grad cast/accumulate,
+// sharded AdamW and the deterministic parameter initialiser.
+//
+// Every kernel moves 16-byte vectors, keeps fp32 statistics, and uses fixed-order
+// (deterministic) reductions except the embedding scatter (fp32 atomics).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ptx.cuh"
+#include "zpp_internal.h"
+
+namespace zpp {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum for blockDim.x == 256 (8 warps); result broadcast to all threads.
+__device__ __forceinline__ float block_sum256(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = (l < 8) ? red[l] : 0.f;
+  t = warp_sum(t);
+  return t;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+  f[0] = bf16lo(u.x); f[1] = bf16hi(u.x); f[2] = bf16lo(u.y); f[3] = bf16hi(u.y);
+  f[4] = bf16lo(u.z); f[5] = bf16hi(u.z); f[6] = bf16lo(u.w); f[7] = bf16hi(u.w);
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+}
+
+// ----------------------------------------------------------------------------
+// LayerNorm: one 256-thread block per row, row cached in registers (cols <= 8192).
+constexpr int LN_VPT = 4;  // uint4 (8 bf16) vectors per thread
+
+__global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                            const bf16* __restrict__ b, bf16* __restrict__ y,
+                                                            float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                            int cols, float eps) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const bf16* xr = x + (long long)row * cols;
+  const int nvec = cols / 8;
+  float v[LN_VPT][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * 256;
+    if (vi < nvec) {
+      unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), v[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[i][j];
+    }
+  }
+  const float mean = block_sum256(s, red) / cols;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * 256;
+    if (vi < nvec) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { const float d = v[i][j] - mean; q += d * d; }
+    }
+  }
+  const float rstd = rsqrtf(block_sum256(q, red) / cols + eps);
+  bf16* yr = y + (long long)row * cols;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * 256;
+    if (vi < nvec) {
+      float gg[8], bb[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg);
+      unpack8(*reinterpret_cast<const uint4*>(b + vi * 8), bb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mean) * rstd * gg[j] + bb[j];
+      *reinterpret_cast<uint4*>(yr + vi * 8) = pack8(o);
+    }
+  }
+  if (threadIdx.x == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid).
+// Each block handles LN_RPB rows and writes per-block column partials of
+// dgamma = sum dy*xhat and dbeta = sum dy (reduced by ln_param_reduce_kernel).
+constexpr int LN_RPB = 8;
+
+__global__ void __launch_bounds__(256) layernorm_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                            const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                            const bf16* __restrict__ g, const bf16* __restrict__ dres,
+                                                            bf16* __restrict__ dx, float* __restrict__ part, int rows,
+                                                            int cols) {
+  __shared__ float red[8];
+  const int nvec = cols / 8;
+  float pg[LN_VPT][8], pb[LN_VPT][8], gg[LN_VPT][8];
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * 256;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { pg[i][j] = 0.f; pb[i][j] = 0.f; gg[i][j] = 0.f; }
+    if (vi < nvec) unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg[i]);
+  }
+  for (int r = 0; r < LN_RPB; ++r) {
+    const int row = blockIdx.x * LN_RPB + r;
+    if (row >= rows) break;
+    const float mu = mean[row], rs = rstd[row];
+    const bf16* xr = x + (long long)row * cols;
+    const bf16* dyr = dy + (long long)row * cols;
+    float xh[LN_VPT][8], dg[LN_VPT][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < LN_VPT; ++i) {
+      const int vi = threadIdx.x + i * 256;
+      if (vi < nvec) {
+        float xv[8], dv[8];
+        unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), xv);
+        unpack8(*reinterpret_cast<const uint4*>(dyr + vi * 8), dv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[i][j] = (xv[j] - mu) * rs;
+          dg[i][j] = dv[j] * gg[i][j];
+          s1 += dg[i][j];
+          s2 += dg[i][j] * xh[i][j];
+          pg[i][j] += dv[j] * xh[i][j];
+          pb[i][j] += dv[j];
+        }
+      }
+    }
+    const float m1 = block_sum256(s1, red) / cols;
+    const float m2 = block_sum256(s2, red) / cols;
+    bf16* dxr = dx + (long long)row * cols;
+#pragma unroll
+    for (int i = 0; i < LN_VPT; ++i) {
+      const int vi = threadIdx.x + i * 256;
+      if (vi < nvec) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = rs * (dg[i][j] - m1 - xh[i][j] * m2);
+        if (dres) {
+          float rv[8];
+          unpack8(*reinterpret_cast<const uint4*>(dres + (long long)row * cols + vi * 8), rv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] += rv[j];
+        }
+        *reinterpret_cast<uint4*>(dxr + vi * 8) = pack8(o);
+      }
+    }
+  }
+  float* pgo = part + (long long)blockIdx.x * 2 * cols;
+  float* pbo = pgo + cols;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * 256;
+    if (vi < nvec) {
+#pragma unroll
+      for (int j = 0; j < 8; j += 4) {
+        *reinterpret_cast<float4*>(pgo + vi * 8 + j) = make_float4(pg[i][j], pg[i][j + 1], pg[i][j + 2], pg[i][j + 3]);
+        *reinterpret_cast<float4*>(pbo + vi * 8 + j) = make_float4(pb[i][j], pb[i][j + 1], pb[i][j + 2], pb[i][j + 3]);
+      }
+    }
+  }
+}
+
+// out_k[c] += sum_b part[b][k*cols + c]  for k in [0, nout)   (fixed order)
+__global__ void partial_reduce_kernel(const float* __restrict__ part, int nblk, int width, float* out0,
+                                      float* out1, int cols) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= width) return;
+  float s = 0.f;
+  for (int b = 0; b < nblk; ++b) s += part[(long long)b * width + c];
+  if (c < cols) out0[c] += s;
+  else out1[c - cols] += s;
+}
+
+// Column sums of a bf16 [rows, cols] matrix (row stride ld): per 64-row block partials.
+constexpr int CS_RPB = 64;
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16* __restrict__ y, long long ld,
+                                                             float* __restrict__ part, int rows, int cols) {
+  const int c8 = blockIdx.x * 256 + threadIdx.x;  // vector of 8 columns
+  if (c8 * 8 >= cols) return;
+  const int r0 = blockIdx.y * CS_RPB;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = r0; r < r0 + CS_RPB && r < rows; ++r) {
+    float v[8];
+    unpack8(*reinterpret_cast<const uint4*>(y + (long long)r * ld + c8 * 8), v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += v[j];
+  }
+  float* o = part + (long long)blockIdx.y * cols + c8 * 8;
+  *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+// ----------------------------------------------------------------------------
+__global__ void gelu_kernel(const bf16* __restrict__ u, bf16* __restrict__ g, long long nvec) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(u)[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = gelu_f(f[j]);
+    reinterpret_cast<uint4*>(g)[i] = pack8(f);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Embedding: out[t] = wte[ids[t]] + wpe[t % seq]
+__global__ void embed_fwd_kernel(const int64_t* __restrict__ ids, const bf16* __restrict__ wte,
+                                 const bf16* __restrict__ wpe, bf16* __restrict__ out, int seq, int hidden) {
+  const int t = blockIdx.x;
+  const long long id = ids[t];
+  const bf16* e = wte + id * hidden;
+  const bf16* p = wpe + (long long)(t % seq) * hidden;
+  bf16* o = out + (long long)t * hidden;
+  for (int v = threadIdx.x; v < hidden / 8; v += blockDim.x) {
+    float a[8], b[8];
+    unpack8(reinterpret_cast<const uint4*>(e)[v], a);
+    unpack8(reinterpret_cast<const uint4*>(p)[v], b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] += b[j];
+    reinterpret_cast<uint4*>(o)[v] = pack8(a);
+  }
+}
+
+__global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, const bf16* __restrict__ dout,
+                                 float* __restrict__ dwte, float* __restrict__ dwpe, int seq, int hidden) {
+  const int t = blockIdx.x;
+  float* e = dwte + ids[t] * (long long)hidden;
+  float* p = dwpe + (long long)(t % seq) * hidden;
+  const bf16* d = dout + (long long)t * hidden;
+  for (int v = threadIdx.x; v < hidden / 8; v += blockDim.x) {
+    float a[8];
+    unpack8(reinterpret_cast<const uint4*>(d)[v], a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      atomicAdd(e + v * 8 + j, a[j]);
+      atomicAdd(p + v * 8 + j, a[j]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Fused softmax cross-entropy, one 256-thread block per row.  Pass 1: online
+// max / sum-exp in fp32; pass 2: dlogits = (softmax - onehot) * scale in place.
+__global__ void __launch_bounds__(256) xent_kernel(bf16* __restrict__ logits, long long ld,
+                                                   const int64_t* __restrict__ labels, float* __restrict__ loss_sum,
+                                                   int vocab, float scale) {
+  __shared__ float sm[8], ss[8];
+  const int row = blockIdx.x;
+  bf16* lr = logits + (long long)row * ld;
+  const int nvec = vocab / 8;
+  float m = -INFINITY, s = 0.f;
+  for (int v = threadIdx.x; v < nvec; v += 256) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(lr)[v], f);
+    float bm = f[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) bm = fmaxf(bm, f[j]);
+    const float nm = fmaxf(m, bm);
+    float acc = s * __expf(m - nm);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += __expf(f[j] - nm);
+    m = nm;
+    s = acc;
+  }
+  // warp reduce (m, s)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(m, om);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sm[w] = m; ss[w] = s; }
+  __syncthreads();
+  float M = sm[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) M = fmaxf(M, sm[i]);
+  float S = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) S += ss[i] * __expf(sm[i] - M);
+  const float lse = M + logf(S);
+  const int lab = static_cast<int>(labels[row]);
+  const float xl = __bfloat162float(lr[lab]);
+  __syncthreads();  // everyone read lr[lab] before it is overwritten
+  if (threadIdx.x == 0) atomicAdd(loss_sum, lse - xl);
+  for (int v = threadIdx.x; v < nvec; v += 256) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(lr)[v], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float p = __expf(f[j] - lse);
+      if (v * 8 + j == lab) p -= 1.f;
+      f[j] = p * scale;
+    }
+    reinterpret_cast<uint4*>(lr)[v] = pack8(f);
+  }
+}
+
+// ----------------------------------------------------------------------------
+__global__ void cast_scale_kernel(const float* __restrict__ in, bf16* __restrict__ out, long long nvec, float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(in)[2 * i];
+    const float4 b = reinterpret_cast<const float4*>(in)[2 * i + 1];
+    const float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale,
+                        b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+    reinterpret_cast<uint4*>(out)[i] = pack8(f);
+  }
+}
+
+__global__ void accum_kernel(const bf16* __restrict__ in, float* __restrict__ acc, long long nvec) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(in)[i], f);
+    float4* a = reinterpret_cast<float4*>(acc) + 2 * i;
+    float4 x = a[0], y = a[1];
+    x.x += f[0]; x.y += f[1]; x.z += f[2]; x.w += f[3];
+    y.x += f[4]; y.y += f[5]; y.z += f[6]; y.w += f[7];
+    a[0] = x;
+    a[1] = y;
+  }
+}
+
+// torch.optim.AdamW semantics: p *= 1 - lr*wd; p -= (lr/bc1) * m / (sqrt(v)/sqrt(bc2) + eps)
+__global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ g, bf16* __restrict__ pb, long long nvec, float lr, float b1,
+                             float b2, float eps, float decay, float step_size, float inv_sqrt_bc2) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    float4 P = reinterpret_cast<float4*>(p)[i], Mv = reinterpret_cast<float4*>(m)[i];
+    float4 Vv = reinterpret_cast<float4*>(v)[i];
+    const float4 G = reinterpret_cast<const float4*>(g)[i];
+    float* pp = &P.x; float* mm = &Mv.x; float* vv = &Vv.x; const float* gg = &G.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mm[j] = b1 * mm[j] + (1.f - b1) * gg[j];
+      vv[j] = b2 * vv[j] + (1.f - b2) * gg[j] * gg[j];
+      pp[j] = pp[j] * decay;
+      pp[j] -= step_size * mm[j] / (sqrtf(vv[j]) * inv_sqrt_bc2 + eps);
+    }
+    reinterpret_cast<float4*>(p)[i] = P;
+    reinterpret_cast<float4*>(m)[i] = Mv;
+    reinterpret_cast<float4*>(v)[i] = Vv;
+    reinterpret_cast<uint2*>(pb)[i] = make_uint2(pack_bf16(P.x, P.y), pack_bf16(P.z, P.w));
+  }
+}
+
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_param_kernel(float* __restrict__ master, bf16* __restrict__ pb, long long n, uint64_t seed,
+                                  long long offset, float mean, float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t base = seed + 4ull * static_cast<uint64_t>(offset + i);
+    float u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u[j] = static_cast<float>(splitmix64(base + j) >> 40) * 5.9604644775390625e-08f;
+    float s = __fadd_rn(__fadd_rn(__fadd_rn(u[0], u[1]), u[2]), u[3]);
+    s = __fsub_rn(s, 2.0f);
+    const float val = __fadd_rn(mean, __fmul_rn(s, scale));
+    master[i] = val;
+    pb[i] = __float2bfloat16_rn(val);
+  }
+}
+
+static int grid_for(long long n, int per_block) {
+  long long g = (n + per_block - 1) / per_block;
+  const long long cap = (long long)num_sms() * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace zpp
+
+using namespace zpp;
+
+#define STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
+                                 int rows, int cols, float eps, uintptr_t stream) {
+  if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
+  if (rows <= 0) return ZPP_OK;
+  layernorm_fwd_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
+                                                          (bf16*)y, mean, rstd, cols, eps);
+  return check_launch("layernorm_fwd");
+}
+
+extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) {
+  return (long long)((rows + LN_RPB - 1) / LN_RPB) * 2 * cols;
+}
+
+extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
+                                 const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
+                                 float* workspace, int rows, int cols, uintptr_t stream) {
+  if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: bad cols");
+  if (rows <= 0) return ZPP_OK;
+  const int nblk = (rows + LN_RPB - 1) / LN_RPB;
+  layernorm_bwd_kernel<<<nblk, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
+                                                          (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx,
+                                                          workspace, rows, cols);
+  int rc = check_launch("layernorm_bwd");
+  if (rc) return rc;
+  partial_reduce_kernel<<<(2 * cols + 255) / 256, 256, 0, STREAM(stream)>>>(workspace, nblk, 2 * cols, dgamma, dbeta,
+                                                                            cols);
+  return check_launch("layernorm_bwd_reduce");
+}
+
+extern "C" int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
+                              uintptr_t stream) {
+  if (cols % 8 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols/ld % 8 != 0");
+  if (rows <= 0) return ZPP_OK;
+  const int nblk = (rows + CS_RPB - 1) / CS_RPB;
+  dim3 grid((cols / 8 + 255) / 256, nblk);
+  colsum_partial_kernel<<<grid, 256, 0, STREAM(stream)>>>((const bf16*)dy, ld, workspace, rows, cols);
+  int rc = check_launch("colsum");
+  if (rc) return rc;
+  partial_reduce_kernel<<<(cols + 255) / 256, 256, 0, STREAM(stream)>>>(workspace, nblk, cols, dbias, dbias, cols);
+  return check_launch("colsum_reduce");
+}
+
+extern "C" int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream) {
+  if (n % 8) return set_error(ZPP_ERR_ARG, "gelu: n % 8 != 0");
+  gelu_kernel<<<grid_for(n / 8, 256), 256, 0, STREAM(stream)>>>((const bf16*)u, (bf16*)g, n / 8);
+  return check_launch("gelu");
+}
+
+extern "C" int zpp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* out, int tokens, int seq,
+                             int hidden, uintptr_t stream) {
+  if (hidden % 8) return set_error(ZPP_ERR_ARG, "embed: hidden % 8 != 0");
+  embed_fwd_kernel<<<tokens, 256, 0, STREAM(stream)>>>(ids, (const bf16*)wte, (const bf16*)wpe, (bf16*)out, seq, hidden);
+  return check_launch("embed_fwd");
+}
+
+extern "C" int zpp_embed_bwd(const int64_t* ids, const void* dout, float* dwte, float* dwpe, int tokens, int seq,
+                             int hidden, uintptr_t stream) {
+  if (hidden % 8) return set_error(ZPP_ERR_ARG, "embed_bwd: hidden % 8 != 0");
+  embed_bwd_kernel<<<tokens, 256, 0, STREAM(stream)>>>(ids, (const bf16*)dout, dwte, dwpe, seq, hidden);
+  return check_launch("embed_bwd");
+}
+
+extern "C" int zpp_xent_fwd_bwd(void* logits, long long ld, const int64_t* labels, float* loss_sum, int rows,
+                                int vocab, float grad_scale, uintptr_t stream) {
+  if (vocab % 8 || ld % 8) return set_error(ZPP_ERR_ARG, "xent: vocab/ld % 8 != 0");
+  xent_kernel<<<rows, 256, 0, STREAM(stream)>>>((bf16*)logits, ld, labels, loss_sum, vocab, grad_scale);
+  return check_launch("xent");
+}
+
+extern "C" int zpp_cast_scale_f32_bf16(const float* in, void* out, long long n, float scale, uintptr_t stream) {
+  if (n % 8) return set_error(ZPP_ERR_ARG, "cast: n % 8 != 0");
+  cast_scale_kernel<<<grid_for(n / 8, 256), 256, 0, STREAM(stream)>>>(in, (bf16*)out, n / 8, scale);
+  return check_launch("cast_scale");
+}
+
+extern "C" int zpp_accum_bf16_f32(const void* in, float* acc, long long n, uintptr_t stream) {
+  if (n % 8) return set_error(ZPP_ERR_ARG, "accum: n % 8 != 0");
+  accum_kernel<<<grid_for(n / 8, 256), 256, 0, STREAM(stream)>>>((const bf16*)in, acc, n / 8);
+  return check_launch("accum");
+}
+
+extern "C" int zpp_adamw(float* master, float* exp_avg, float* exp_avg_sq, const float* grad, void* param_bf16,
+                         long long n, float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                         uintptr_t stream) {
+  if (n % 4) return set_error(ZPP_ERR_ARG, "adamw: n % 4 != 0");
+  if (step < 1) return set_error(ZPP_ERR_ARG, "adamw: step must be >= 1");
+  const double bc1 = 1.0 - pow((double)beta1, step), bc2 = 1.0 - pow((double)beta2, step);
+  adamw_kernel<<<grid_for(n / 4, 256), 256, 0, STREAM(stream)>>>(
+      master, exp_avg, exp_avg_sq, grad, (bf16*)param_bf16, n / 4, lr, beta1, beta2, eps, 1.f - lr * weight_decay,
+      (float)(lr / bc1), (float)(1.0 / sqrt(bc2)));
+  return check_launch("adamw");
+}
+
+extern "C" int zpp_init_param(float* master, void* param_bf16, long long n, unsigned long long seed, long long offset,
+                              float mean, float std, uintptr_t stream) {
+  const float scale = std * 1.7320508075688772f;
+  init_param_kernel<<<grid_for(n, 256), 256, 0, STREAM(stream)>>>(master, (bf16*)param_bf16, n, seed, offset, mean,
+                                                                  scale);
+  return check_launch("init_param");
+}

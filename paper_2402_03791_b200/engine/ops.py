@@ -1,0 +1,118 @@
+"""Tensor-level wrappers over the libzpp C ABI.
+
+torch tensors are used only as device-memory handles (``data_ptr``) and for
+stream plumbing; every operation below is one of our sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import lib
+from .lib import EPI_BF16, EPI_BF16_DGELU, EPI_BF16_GELU, EPI_F32, EPI_F32_ACC  # noqa: F401
+
+
+def _s(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def _p(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _ld(t: torch.Tensor) -> int:
+    assert t.dim() == 2 and t.stride(1) == 1, "2-D row-major (unit inner stride) tensor expected"
+    return t.stride(0)
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_t: bool = False, b_t: bool = False,
+         epilogue: int = EPI_BF16, bias=None, resid=None, aux=None, stream=None) -> torch.Tensor:
+    """c[M,N] (op)= A @ B^T with A = a (M x K) or a^T (a is K x M, ``a_t``),
+    B = b (N x K) or b^T (b is K x N, ``b_t``)."""
+    M = a.shape[1] if a_t else a.shape[0]
+    K = a.shape[0] if a_t else a.shape[1]
+    N = b.shape[1] if b_t else b.shape[0]
+    assert (b.shape[0] if b_t else b.shape[1]) == K, "inner dimensions differ"
+    assert c.shape[0] == M and c.shape[1] == N
+    lib.call("zpp_gemm", _p(a), int(a_t), _ld(a), _p(b), int(b_t), _ld(b), _p(c), _ld(c), M, N, K,
+             epilogue, _p(bias), _p(resid), _ld(resid) if resid is not None else 0,
+             _p(aux), _ld(aux) if aux is not None else 0, _s(stream))
+    return c
+
+
+def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    lib.call("zpp_layernorm_fwd", _p(x), _p(gamma), _p(beta), _p(y), _p(mean), _p(rstd), rows, cols,
+             eps, _s(stream))
+
+
+def layernorm_bwd_workspace(rows: int, cols: int) -> int:
+    return lib.load().zpp_layernorm_bwd_workspace_floats(rows, cols)
+
+
+def layernorm_bwd(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, workspace, dresid=None, stream=None):
+    rows, cols = x.shape
+    lib.call("zpp_layernorm_bwd", _p(dy), _p(x), _p(mean), _p(rstd), _p(gamma), _p(dresid), _p(dx),
+             _p(dgamma), _p(dbeta), _p(workspace), rows, cols, _s(stream))
+
+
+def colsum_acc(dy, dbias, workspace, stream=None):
+    rows, cols = dy.shape
+    lib.call("zpp_colsum_acc", _p(dy), _ld(dy), _p(dbias), _p(workspace), rows, cols, _s(stream))
+
+
+def colsum_workspace(rows: int, cols: int) -> int:
+    return ((rows + 63) // 64) * cols
+
+
+def gelu(u, g, stream=None):
+    lib.call("zpp_gelu_fwd", _p(u), _p(g), u.numel(), _s(stream))
+
+
+def attn_fwd(qkv, out, lse, batch, seq, heads, head_dim, stream=None):
+    lib.call("zpp_attn_fwd", _p(qkv), _p(out), _p(lse), batch, seq, heads, head_dim, _s(stream))
+
+
+def attn_bwd_workspace(batch, seq, heads, head_dim) -> int:
+    return lib.load().zpp_attn_bwd_workspace_floats(batch, seq, heads, head_dim)
+
+
+def attn_bwd(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, head_dim, stream=None):
+    lib.call("zpp_attn_bwd", _p(qkv), _p(out), _p(lse), _p(dout), _p(dqkv), _p(workspace), batch, seq,
+             heads, head_dim, _s(stream))
+
+
+def embed_fwd(ids, wte, wpe, out, seq, stream=None):
+    tokens, hidden = out.shape
+    lib.call("zpp_embed_fwd", _p(ids), _p(wte), _p(wpe), _p(out), tokens, seq, hidden, _s(stream))
+
+
+def embed_bwd(ids, dout, dwte, dwpe, seq, stream=None):
+    tokens, hidden = dout.shape
+    lib.call("zpp_embed_bwd", _p(ids), _p(dout), _p(dwte), _p(dwpe), tokens, seq, hidden, _s(stream))
+
+
+def xent(logits, labels, loss_sum, grad_scale, stream=None):
+    rows, vocab = logits.shape
+    lib.call("zpp_xent_fwd_bwd", _p(logits), _ld(logits), _p(labels), _p(loss_sum), rows, vocab,
+             grad_scale, _s(stream))
+
+
+def cast_scale(src_f32, dst_bf16, scale=1.0, stream=None):
+    lib.call("zpp_cast_scale_f32_bf16", _p(src_f32), _p(dst_bf16), src_f32.numel(), scale, _s(stream))
+
+
+def accum(src_bf16, acc_f32, stream=None):
+    lib.call("zpp_accum_bf16_f32", _p(src_bf16), _p(acc_f32), src_bf16.numel(), _s(stream))
+
+
+def adamw(master, m, v, grad, param_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
+    lib.call("zpp_adamw", _p(master), _p(m), _p(v), _p(grad), _p(param_bf16), master.numel(), lr, beta1,
+             beta2, eps, wd, step, _s(stream))
+
+
+def init_param(master, param_bf16, seed, offset, mean, std, stream=None):
+    lib.call("zpp_init_param", _p(master), _p(param_bf16), master.numel(), seed, offset, mean, std,
+             _s(stream))

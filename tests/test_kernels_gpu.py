@@ -1,0 +1,228 @@
+"""Numerics of every libzpp kernel against a plain PyTorch fp32 reference (B200 only).
+
+Tolerances: bf16-output kernels are compared to the fp32 reference with
+|err| <= atol + rtol*|ref| (rtol 2e-2, atol scaled to the output magnitude);
+fp32-output GEMMs to 1e-2 relative Frobenius error; the initialiser is
+bit-exact against the numpy restatement in oracle/init_oracle.py.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2402_03791_b200.engine import ops  # noqa: E402
+
+dev = "cuda"
+
+
+def rel_err(x, ref):
+    return ((x.float() - ref).norm() / ref.norm().clamp_min(1e-12)).item()
+
+
+def bf(*shape, scale=1.0, gen=None):
+    return (torch.randn(*shape, device=dev, generator=gen) * scale).to(torch.bfloat16)
+
+
+@pytest.fixture(autouse=True)
+def _seed():
+    torch.manual_seed(0)
+
+
+GEMM_SHAPES = [(128, 128, 64), (256, 512, 256), (200, 136, 72), (384, 1024, 320), (2048, 3072, 1024),
+               (128, 50304, 256), (1000, 264, 4096)]
+
+
+@pytest.mark.parametrize("a_t", [False, True])
+@pytest.mark.parametrize("b_t", [False, True])
+@pytest.mark.parametrize("shape", GEMM_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_gemm_layouts(shape, a_t, b_t):
+    M, N, K = shape
+    if (a_t and M % 8) or (b_t and N % 8):
+        pytest.skip("MN-major operands need 16-byte row pitch")
+    A = bf(M, K)
+    B = bf(N, K)
+    a = A.t().contiguous() if a_t else A
+    b = B.t().contiguous() if b_t else B
+    C = torch.empty(M, N, device=dev, dtype=torch.float32)
+    ops.gemm(a, b, C, a_t=a_t, b_t=b_t, epilogue=ops.EPI_F32)
+    ref = A.float() @ B.float().t()
+    torch.cuda.synchronize()
+    assert rel_err(C, ref) < 1e-5 * math.sqrt(K) + 1e-5
+
+
+def test_gemm_bf16_bias_resid():
+    M, N, K = 512, 768, 256
+    A, B = bf(M, K), bf(N, K)
+    bias, resid = bf(N), bf(M, N)
+    C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    ops.gemm(A, B, C, bias=bias, resid=resid)
+    ref = A.float() @ B.float().t() + bias.float() + resid.float()
+    assert rel_err(C, ref) < 1e-2
+
+
+def test_gemm_gelu_and_dgelu():
+    M, N, K = 256, 1024, 512
+    A, B, bias = bf(M, K, scale=0.5), bf(N, K, scale=0.1), bf(N)
+    G = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    U = torch.empty_like(G)
+    ops.gemm(A, B, G, epilogue=ops.EPI_BF16_GELU, bias=bias, aux=U)
+    u_ref = A.float() @ B.float().t() + bias.float()
+    assert rel_err(U, u_ref) < 1e-2
+    g_ref = torch.nn.functional.gelu(U.float(), approximate="tanh")
+    assert rel_err(G, g_ref) < 1e-2
+    # dgelu: C = (A B^T) * gelu'(U)
+    D = torch.empty_like(G)
+    ops.gemm(A, B, D, epilogue=ops.EPI_BF16_DGELU, aux=U)
+    u = U.float().requires_grad_(True)
+    gy = A.float() @ B.float().t()
+    torch.nn.functional.gelu(u, approximate="tanh").backward(gy)
+    assert rel_err(D, u.grad) < 1e-2
+
+
+def test_gemm_f32_accumulate():
+    M, N, K = 384, 256, 512
+    A, B = bf(K, M), bf(K, N)  # wgrad layout: both MN-major
+    C = torch.randn(M, N, device=dev)
+    ref = C.clone() + A.float().t() @ B.float()
+    ops.gemm(A, B, C, a_t=True, b_t=True, epilogue=ops.EPI_F32_ACC)
+    assert rel_err(C, ref) < 1e-5
+
+
+@pytest.mark.parametrize("cols", [256, 2048, 4096])
+def test_layernorm(cols):
+    rows = 300
+    x = bf(rows, cols, scale=2.0) + 0.5
+    g, b = bf(cols) + 1.0, bf(cols, scale=0.1)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=dev)
+    rstd = torch.empty(rows, device=dev)
+    ops.layernorm_fwd(x, g, b, y, mean, rstd)
+    xf = x.float().requires_grad_(True)
+    gf = g.float().requires_grad_(True)
+    bff = b.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xf, (cols,), gf, bff, 1e-5)
+    assert rel_err(y, yr) < 1e-2
+    dy = bf(rows, cols)
+    dres = bf(rows, cols)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(cols, device=dev)
+    db = torch.zeros(cols, device=dev)
+    ws = torch.empty(ops.layernorm_bwd_workspace(rows, cols), device=dev)
+    ops.layernorm_bwd(dy, x, mean, rstd, g, dx, dg, db, ws, dresid=dres)
+    assert rel_err(dx, xf.grad + dres.float()) < 1e-2
+    assert rel_err(dg, gf.grad) < 1e-4
+    assert rel_err(db, bff.grad) < 1e-4
+
+
+def test_colsum():
+    dy = bf(1000, 768)
+    acc = torch.randn(768, device=dev)
+    ref = acc + dy.float().sum(0)
+    ws = torch.empty(ops.colsum_workspace(1000, 768), device=dev)
+    ops.colsum_acc(dy, acc, ws)
+    assert rel_err(acc, ref) < 1e-5
+
+
+def _attn_ref(qkv, b, s, H, D):
+    q, k, v = qkv.float().view(b, s, 3, H, D).unbind(2)
+    q, k, v = (t.transpose(1, 2) for t in (q, k, v))  # b H s D
+    att = (q @ k.transpose(-1, -2)) / math.sqrt(D)
+    mask = torch.ones(s, s, device=dev, dtype=torch.bool).triu(1)
+    att = att.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(att, -1)
+    o = torch.softmax(att, -1) @ v
+    return o.transpose(1, 2).reshape(b * s, H * D), lse
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("b,s,H", [(1, 128, 2), (2, 256, 3)])
+def test_attention(b, s, H, D):
+    qkv = bf(b * s, 3 * H * D)
+    out = torch.empty(b * s, H * D, device=dev, dtype=torch.bfloat16)
+    lse = torch.empty(b, H, s, device=dev)
+    ops.attn_fwd(qkv, out, lse, b, s, H, D)
+    qf = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = _attn_ref(qf, b, s, H, D)
+    assert rel_err(out, o_ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 1e-2
+    do = bf(b * s, H * D)
+    o_ref.backward(do.float())
+    dqkv = torch.empty_like(qkv)
+    ws = torch.empty(ops.attn_bwd_workspace(b, s, H, D), device=dev)
+    ops.attn_bwd(qkv, out, lse, do, dqkv, ws, b, s, H, D)
+    g = qf.grad.view(b * s, 3, H * D)
+    d = dqkv.view(b * s, 3, H * D)
+    for i in range(3):
+        assert rel_err(d[:, i], g[:, i]) < 2e-2, f"slot {i}"
+
+
+def test_embedding():
+    V, S, Hd, T = 1000, 64, 256, 128
+    wte, wpe = bf(V, Hd), bf(S, Hd)
+    ids = torch.randint(0, V, (T,), device=dev)
+    out = torch.empty(T, Hd, device=dev, dtype=torch.bfloat16)
+    ops.embed_fwd(ids, wte, wpe, out, S)
+    ref = wte.float()[ids] + wpe.float()[torch.arange(T, device=dev) % S]
+    assert rel_err(out, ref) < 1e-2
+    dout = bf(T, Hd)
+    dwte = torch.zeros(V, Hd, device=dev)
+    dwpe = torch.zeros(S, Hd, device=dev)
+    ops.embed_bwd(ids, dout, dwte, dwpe, S)
+    rwte = torch.zeros(V, Hd, device=dev).index_add_(0, ids, dout.float())
+    rwpe = torch.zeros(S, Hd, device=dev).index_add_(0, torch.arange(T, device=dev) % S, dout.float())
+    assert rel_err(dwte, rwte) < 1e-5 and rel_err(dwpe, rwpe) < 1e-5
+
+
+@pytest.mark.parametrize("V", [512, 50304])
+def test_cross_entropy(V):
+    rows = 64
+    logits = bf(rows, V, scale=3.0)
+    labels = torch.randint(0, V, (rows,), device=dev)
+    lf = logits.float().requires_grad_(True)
+    loss_ref = torch.nn.functional.cross_entropy(lf, labels, reduction="sum")
+    loss_ref.backward()
+    loss = torch.zeros(1, device=dev)
+    buf = logits.clone()
+    ops.xent(buf, labels, loss, 1.0)
+    assert abs(loss.item() - loss_ref.item()) / loss_ref.item() < 1e-4
+    assert rel_err(buf, lf.grad) < 1e-2
+
+
+def test_cast_accum_adamw():
+    n = 4096 * 3
+    g = torch.randn(n, device=dev)
+    w = torch.empty(n, device=dev, dtype=torch.bfloat16)
+    ops.cast_scale(g, w, 0.5)
+    assert torch.equal(w, (g * 0.5).to(torch.bfloat16))
+    acc = torch.randn(n, device=dev)
+    ref = acc + w.float()
+    ops.accum(w, acc)
+    assert torch.allclose(acc, ref)
+    p = torch.randn(n, device=dev)
+    m, v = torch.zeros(n, device=dev), torch.zeros(n, device=dev)
+    pb = torch.empty(n, device=dev, dtype=torch.bfloat16)
+    pt = p.clone().requires_grad_(True)
+    opt = torch.optim.AdamW([pt], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    for step in range(1, 4):
+        grad = torch.randn(n, device=dev)
+        ops.adamw(p, m, v, grad, pb, 1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        pt.grad = grad.clone()
+        opt.step()
+    assert (p - pt.detach()).abs().max().item() < 1e-6
+    assert torch.equal(pb, p.to(torch.bfloat16))
+
+
+def test_init_param_bit_exact():
+    from oracle.init_oracle import init_values
+    n = 100003
+    master = torch.empty(n + 1, device=dev)[:n]
+    pb = torch.empty(n, device=dev, dtype=torch.bfloat16)
+    ops.init_param(master, pb, 1234, 777, 0.0, 0.02)
+    ref = init_values(n, 1234, 777, 0.0, 0.02)
+    assert np.array_equal(master.cpu().numpy(), ref)
+    assert torch.equal(pb.cpu(), torch.from_numpy(ref).to(torch.bfloat16))
