@@ -40,6 +40,9 @@ const char* zpp_last_error(void);
 int zpp_num_sms(void);
 int zpp_version(void);
 
+/* cudaMemsetAsync(ptr, 0, bytes) on stream (grad buffers, loss accumulator) */
+int zpp_zero(void* ptr, long long bytes, uintptr_t stream);
+
 /* ---- dense contractions (tcgen05 / TMEM / TMA) -------------------------------
  * Replaces the cost of F/B/W tasks (schedules.py:51-66).
  * C[M,N] (op)= sum_k A(m,k) B(n,k); A is K-major (A[m*lda+k]) or M-major

@@ -75,3 +75,8 @@ int encode_tensor_map(CUtensorMap* map, CUtensorMapDataType dtype, int rank, voi
 extern "C" const char* zpp_last_error(void) { return zpp::g_err; }
 extern "C" int zpp_num_sms(void) { return zpp::num_sms(); }
 extern "C" int zpp_version(void) { return 1; }
+
+extern "C" int zpp_zero(void* ptr, long long bytes, uintptr_t stream) {
+  cudaError_t e = cudaMemsetAsync(ptr, 0, (size_t)bytes, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? ZPP_OK : zpp::set_cuda_error(e, "zpp_zero");
+}

@@ -1,0 +1,483 @@
+"""Per-rank ZeroPP step executor: the real-hardware replacement for the
+reference's ``simulate`` (`pkg/src/zeroppsim/simulation.py:90-158`).
+
+One OS process per GPU; rank r is pipeline rank p = r // D and ZeRO index
+z = r % D.  The host walks ``sched.per_device[p]`` in order and only enqueues
+work; ordering across streams uses CUDA events:
+
+    compute    F / B / W (GPT stage math, libzpp kernels), OPT (sharded AdamW)
+    ag         AG_PARAM: ncclAllGather of the stage's bf16 shard (in place)
+    rs         RS_GRAD : fp32 stage grad -> bf16 wire -> ncclReduceScatter -> += fp32 shard grad
+    act_send / act_recv / grad_send / grad_recv: stage-boundary P2P
+
+P2P uses one dedicated 2-rank communicator per (message kind, directed pair):
+NCCL matches send/recv by order only, and a shared channel would swap
+activations and gradients.  The ZeRO group uses two
+communicators (one per stream) so all-gathers and reduce-scatters never share
+a communicator across streams.
+
+Task semantics follow the reference schedule exactly (task order from
+`schedules.py:339-474`; edges `schedules.py:98-163`); the executor asserts the
+schedule validates (`validation.py:99-135`) before touching the GPU.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from ..config import HybridMode, ModelSpec, ParallelConfig, Placement, RecomputeMode
+from ..tasks import Schedule, Task, TaskKind
+from ..validation import validate
+from . import lib, ops
+from .model import GPTSpec, StageLayout, init_offset, shard_init_ranges, stage_layout
+
+BF16, F32 = torch.bfloat16, torch.float32
+
+
+@dataclass
+class StepResult:
+    """SimResult-shaped measurement of one executed step on this rank
+    (fields mirror `simulation.py:53-77`, times in milliseconds)."""
+
+    loss_sum: torch.Tensor                  # device scalar: sum of CE over this rank's tokens
+    tokens: int                             # tokens processed by this rank's last stage
+    step_ms: float | None = None
+    task_times: dict = field(default_factory=dict)
+    exposed_comm_ms: float | None = None    # compute-stream waits on AG / RS
+    p2p_wait_ms: float | None = None        # compute-stream waits on P2P recv (bubble + transfer)
+    busy_ms: float | None = None
+
+
+class _Stage:
+    """Buffers and views of one pipeline stage held by this rank."""
+
+    def __init__(self, lay: StageLayout, D: int, z: int, dev):
+        self.lay = lay
+        n, ns = lay.numel, lay.shard_numel
+        self.gathered = torch.zeros(n, dtype=BF16, device=dev)
+        self.shard_bf16 = self.gathered[z * ns:(z + 1) * ns]      # in-place all-gather layout
+        self.master = torch.zeros(ns, dtype=F32, device=dev)
+        self.exp_avg = torch.zeros(ns, dtype=F32, device=dev)
+        self.exp_avg_sq = torch.zeros(ns, dtype=F32, device=dev)
+        self.grad_shard = torch.zeros(ns, dtype=F32, device=dev)
+        self.grad_full = self.grad_shard if D == 1 else torch.zeros(n, dtype=F32, device=dev)
+        self.p: dict = {}
+        self.g: dict = {}
+        for s in lay.slots:
+            key = (s.name, s.layer)
+            self.p[key] = self.gathered[s.offset:s.offset + s.numel].view(*s.shape)
+            self.g[key] = self.grad_full[s.offset:s.offset + s.numel].view(*s.shape)
+        self.ag_event = None        # compute must wait before using gathered params
+        self.grad_free_event = None  # compute must wait before writing grad_full again
+
+
+class Runtime:
+    """Everything one rank needs to execute ZeroPP steps for a fixed config."""
+
+    def __init__(self, spec: GPTSpec, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
+                 sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
+                 timeline: bool = False):
+        if world != cfg.pp_size * cfg.dp_size:
+            raise ValueError(f"world size {world} != P*D = {cfg.pp_size * cfg.dp_size}")
+        if model.num_layers != spec.num_layers or model.hidden_size != spec.hidden or \
+                model.seq_len != spec.seq_len:
+            raise ValueError("ModelSpec and GPTSpec disagree on L / h / s")
+        if cfg.microbatch_samples != spec.microbatch_samples:
+            raise ValueError("ParallelConfig.microbatch_samples != GPTSpec.microbatch_samples")
+        if cfg.recompute is RecomputeMode.FULL and cfg.stages_per_device > 1:
+            raise NotImplementedError("recompute=full (R tasks) is a 'next' row (SURVEY.md 8f)")
+        if cfg.inter_node_dp > 1:
+            raise NotImplementedError("inter_node_dp > 1 (outer DP / ZeRO-1) is a 'next' row")
+        bad = validate(sched, placement, cfg)
+        if bad:
+            raise ValueError(f"schedule failed validation: {bad[0]}")
+        self.spec, self.model, self.cfg, self.pl, self.sched = spec, model, cfg, placement, sched
+        self.rank, self.world = rank, world
+        self.P, self.D = cfg.pp_size, cfg.dp_size
+        self.p, self.z = rank // self.D, rank % self.D
+        self.S = cfg.num_stages
+        self.timeline = timeline
+        if device is None:
+            device = torch.cuda.current_device()
+        self.dev = torch.device("cuda", device)
+        torch.cuda.set_device(self.dev)
+        lib.load()
+        self.tasks = list(sched.per_device[self.p])
+        self.local_stages = placement.device_stages(self.p)
+        self.stages: dict[int, _Stage] = {}
+        for s in self.local_stages:
+            lay = stage_layout(spec, s, self.S, placement.stage_to_layers[s], self.D)
+            self.stages[s] = _Stage(lay, self.D, self.z, self.dev)
+        mk = lambda: torch.cuda.Stream(device=self.dev)  # noqa: E731
+        self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
+        self.s_act_send, self.s_act_recv, self.s_grad_send, self.s_grad_recv = mk(), mk(), mk(), mk()
+        T, h = spec.tokens_per_microbatch, spec.hidden
+        self.ln_ws = torch.empty(ops.layernorm_bwd_workspace(T, h), dtype=F32, device=self.dev)
+        self.cs_ws = torch.empty(ops.colsum_workspace(T, 4 * h), dtype=F32, device=self.dev)
+        self.attn_ws = torch.empty(ops.attn_bwd_workspace(spec.microbatch_samples, spec.seq_len,
+                                                          spec.heads, spec.head_dim),
+                                   dtype=F32, device=self.dev)
+        max_n = max(st.lay.numel for st in self.stages.values())
+        max_ns = max(st.lay.shard_numel for st in self.stages.values())
+        if self.D > 1:
+            self.rs_send = torch.empty(max_n, dtype=BF16, device=self.dev)
+            self.rs_recv = torch.empty(max_ns, dtype=BF16, device=self.dev)
+        self.loss_sum = torch.zeros(1, dtype=F32, device=self.dev)
+        self.step_count = 0
+        self.opt_event = None
+        self.comms: dict = {}
+        if world > 1:
+            self._init_comms()
+        self.init_params()
+
+    # ------------------------------------------------------------------ setup
+    def _init_comms(self) -> None:
+        """Create ZeRO and P2P communicators in one global order (no init deadlock)."""
+        import torch.distributed as dist
+        lib.load_nccl()
+        P, D = self.P, self.D
+        plan = []  # (key, ranks)
+        for p in range(P):
+            grp = [p * D + z for z in range(D)]
+            if D > 1:
+                plan.append((("ag", p), grp))
+                plan.append((("rs", p), grp))
+        if P > 1:
+            for z in range(D):
+                for p in range(P):
+                    nxt, prv = (p + 1) % P, (p - 1) % P
+                    plan.append((("act", p, nxt, z), [p * D + z, nxt * D + z]))
+                    plan.append((("grad", p, prv, z), [p * D + z, prv * D + z]))
+        import ctypes
+        uids = []
+        if self.rank == 0:
+            for _ in plan:
+                b = ctypes.create_string_buffer(128)
+                lib.call("zpp_nccl_unique_id", b)
+                uids.append(b.raw)
+        obj = [uids]
+        dist.broadcast_object_list(obj, src=0)
+        uids = obj[0]
+        for (key, ranks), uid in zip(plan, uids):
+            if self.rank in ranks:
+                handle = ctypes.c_void_p()
+                lib.call("zpp_comm_init", uid, len(ranks), ranks.index(self.rank), ctypes.byref(handle))
+                self.comms[key] = handle
+
+    def init_params(self) -> None:
+        """Deterministic init of this rank's shards (identical for every P x D split)."""
+        with torch.cuda.stream(self.s_comp):
+            for st in self.stages.values():
+                for slot, t0, s0, cnt in shard_init_ranges(st.lay, self.z):
+                    ops.init_param(st.master[s0:s0 + cnt], st.shard_bf16[s0:s0 + cnt], self.spec.seed,
+                                   init_offset(slot.uid) + t0, slot.mean, slot.std, stream=self.s_comp)
+        self.opt_event = self._record(self.s_comp)
+        if self.D == 1:
+            for st in self.stages.values():
+                st.ag_event = None
+
+    # ------------------------------------------------------------------ helpers
+    @staticmethod
+    def _record(stream, timing: bool = False):
+        ev = torch.cuda.Event(enable_timing=timing)
+        ev.record(stream)
+        return ev
+
+    def _wait(self, ev, kind: str | None = None):
+        """Make the compute stream wait on ``ev``; measure the stall if timing."""
+        if ev is None:
+            return
+        if self.timeline and kind is not None:
+            e0 = self._record(self.s_comp, True)
+            self.s_comp.wait_event(ev)
+            e1 = self._record(self.s_comp, True)
+            self._waits.append((kind, e0, e1))
+        else:
+            self.s_comp.wait_event(ev)
+
+    def _dev_of(self, s: int) -> int:
+        return self.pl.stage_to_device[s]
+
+    def _peer_rank(self, p: int) -> int:
+        return p * self.D + self.z
+
+    # ------------------------------------------------------------------ step
+    def step(self, ids: torch.Tensor, labels: torch.Tensor) -> StepResult:
+        """Execute one step.  ``ids`` / ``labels``: contiguous int64 [B, b*s] device
+        tensors holding this ZeRO rank's micro-batches (labels = next tokens)."""
+        spec, cfg = self.spec, self.cfg
+        B, b, s_len = cfg.microbatches, spec.microbatch_samples, spec.seq_len
+        assert ids.shape == (B, b * s_len) and labels.shape == (B, b * s_len)
+        self._ids, self._labels = ids, labels
+        self._stash: dict = {}
+        self._local_act: dict = {}
+        self._local_grad: dict = {}
+        self._waits: list = []
+        self._rs_events: list = []
+        self._grad_scale = 1.0 / (self.D * B * b * s_len)
+        self.step_count += 1
+        times = {}
+        comp = self.s_comp
+        comp.wait_stream(torch.cuda.current_stream(self.dev))
+        t_start = self._record(comp, True)
+        with torch.cuda.stream(comp):
+            ops.zero(self.loss_sum, stream=comp)
+            for task in self.tasks:
+                stream = self._stream_of(task)
+                e0 = self._record(stream, True) if self.timeline else None
+                self._run(task)
+                if self.timeline:
+                    times[task] = (e0, self._record(stream, True))
+        t_end = self._record(comp, True)
+        torch.cuda.current_stream(self.dev).wait_stream(comp)
+        self._t = (t_start, t_end, times)
+        tokens_done = B * b * s_len if (self.S - 1) in self.stages else 0
+        return StepResult(self.loss_sum, tokens_done)
+
+    def finish_timing(self, res: StepResult) -> StepResult:
+        """Resolve CUDA-event timings of the last step (synchronizes)."""
+        torch.cuda.synchronize(self.dev)
+        t_start, t_end, times = self._t
+        res.step_ms = t_start.elapsed_time(t_end)
+        if self.timeline:
+            res.task_times = {t: (t_start.elapsed_time(a), t_start.elapsed_time(b)) for t, (a, b) in times.items()}
+            res.busy_ms = sum(e - s for t, (s, e) in res.task_times.items() if t.is_compute)
+            res.exposed_comm_ms = sum(a.elapsed_time(b) for k, a, b in self._waits if k == "zero")
+            res.p2p_wait_ms = sum(a.elapsed_time(b) for k, a, b in self._waits if k == "p2p")
+        return res
+
+    def _stream_of(self, task: Task):
+        if task.kind is TaskKind.AG_PARAM:
+            return self.s_ag
+        if task.kind is TaskKind.RS_GRAD:
+            return self.s_rs
+        return self.s_comp
+
+    def _run(self, task: Task) -> None:
+        k = task.kind
+        if k is TaskKind.F:
+            self._forward(task.stage, task.microbatch)
+        elif k is TaskKind.B:
+            self._backward_input(task.stage, task.microbatch)
+        elif k is TaskKind.W:
+            self._backward_weight(task.stage, task.microbatch)
+        elif k is TaskKind.AG_PARAM:
+            self._all_gather(task.stage)
+        elif k is TaskKind.RS_GRAD:
+            self._reduce_scatter(task.stage)
+        elif k is TaskKind.OPT:
+            self._optimizer()
+        elif k in (TaskKind.RS_GRAD_INTER, TaskKind.AG_PARAM_INTER, TaskKind.AR_GRAD):
+            if task.bytes:
+                raise NotImplementedError("outer (inter-node) collectives are a 'next' row")
+        else:
+            raise NotImplementedError(f"task kind {k}")
+
+    # ------------------------------------------------------------------ comm tasks
+    def _all_gather(self, s: int) -> None:
+        st = self.stages[s]
+        if self.D == 1:
+            st.ag_event = None
+            return
+        self.s_ag.wait_event(self.opt_event)  # shards are final once the previous OPT ran
+        ns = st.lay.shard_numel
+        lib.call("zpp_allgather", self.comms[("ag", self.p)], st.shard_bf16.data_ptr(),
+                 st.gathered.data_ptr(), ns, 0, self.s_ag.cuda_stream)
+        st.ag_event = self._record(self.s_ag)
+
+    def _reduce_scatter(self, s: int) -> None:
+        st = self.stages[s]
+        if self.D == 1:
+            return  # the stage grad IS the shard grad; nothing moves (0 bytes)
+        rs = self.s_rs
+        rs.wait_event(self._record(self.s_comp))   # all B/W of (s, u) enqueued before this point
+        n, ns = st.lay.numel, st.lay.shard_numel
+        send, recv = self.rs_send[:n], self.rs_recv[:ns]
+        ops.cast_scale(st.grad_full, send, 1.0, stream=rs)
+        ops.zero(st.grad_full, stream=rs)
+        st.grad_free_event = self._record(rs)
+        lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], send.data_ptr(), recv.data_ptr(), ns, 0,
+                 rs.cuda_stream)
+        ops.accum(recv, st.grad_shard, stream=rs)
+        self._rs_events.append(self._record(rs))
+
+    def _optimizer(self) -> None:
+        for ev in self._rs_events:
+            self._wait(ev, "zero")
+        spec = self.spec
+        for st in self.stages.values():
+            ops.adamw(st.master, st.exp_avg, st.exp_avg_sq, st.grad_shard, st.shard_bf16, spec.lr, spec.beta1,
+                      spec.beta2, spec.adam_eps, spec.weight_decay, self.step_count, stream=self.s_comp)
+        if self.capture_grads:
+            self.captured = {s: st.grad_shard.clone() for s, st in self.stages.items()}
+        for st in self.stages.values():
+            ops.zero(st.grad_shard, stream=self.s_comp)
+        self.opt_event = self._record(self.s_comp)
+
+    capture_grads = False
+    captured: dict = {}
+
+    def _use_params(self, st: _Stage) -> None:
+        if st.ag_event is not None:
+            self._wait(st.ag_event, "zero")
+            st.ag_event = None
+
+    def _touch_grads(self, st: _Stage) -> None:
+        if st.grad_free_event is not None:
+            self._wait(st.grad_free_event, "zero")
+            st.grad_free_event = None
+
+    # P2P ---------------------------------------------------------------------
+    def _send(self, kind: str, t: torch.Tensor, to_p: int) -> None:
+        stream = self.s_act_send if kind == "act" else self.s_grad_send
+        stream.wait_event(self._record(self.s_comp))
+        lib.call("zpp_send", self.comms[(kind, self.p, to_p, self.z)], t.data_ptr(), t.numel(), 0, 1,
+                 stream.cuda_stream)
+        t.record_stream(stream)
+
+    def _recv(self, kind: str, shape, from_p: int) -> torch.Tensor:
+        stream = self.s_act_recv if kind == "act" else self.s_grad_recv
+        with torch.cuda.stream(stream):
+            buf = torch.empty(*shape, dtype=BF16, device=self.dev)
+        lib.call("zpp_recv", self.comms[(kind, from_p, self.p, self.z)], buf.data_ptr(), buf.numel(), 0, 0,
+                 stream.cuda_stream)
+        self._wait(self._record(stream), "p2p")
+        buf.record_stream(self.s_comp)
+        return buf
+
+    # ------------------------------------------------------------------ stage math
+    def _forward(self, s: int, m: int) -> None:
+        spec = self.spec
+        st = self.stages[s]
+        self._use_params(st)
+        T, h, H, dh = spec.tokens_per_microbatch, spec.hidden, spec.heads, spec.head_dim
+        b, sl = spec.microbatch_samples, spec.seq_len
+        P = st.p
+        e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
+        if s == 0:
+            x = e(T, h)
+            ops.embed_fwd(self._ids[m], P[("wte", None)], P[("wpe", None)], x, sl)
+        elif self._dev_of(s - 1) == self.p:
+            x = self._local_act.pop((s, m))
+        else:
+            x = self._recv("act", (T, h), self._dev_of(s - 1))
+        layers = []
+        lo, hi = st.lay.layers
+        for l in range(lo, hi):
+            xn1, mu1, r1 = e(T, h), e(T, dt=F32), e(T, dt=F32)
+            ops.layernorm_fwd(x, P[("ln1_g", l)], P[("ln1_b", l)], xn1, mu1, r1, spec.ln_eps)
+            qkv = e(T, 3 * h)
+            ops.gemm(xn1, P[("w_qkv", l)], qkv, bias=P[("b_qkv", l)])
+            o, lse = e(T, h), e(b, H, sl, dt=F32)
+            ops.attn_fwd(qkv, o, lse, b, sl, H, dh)
+            x1 = e(T, h)
+            ops.gemm(o, P[("w_proj", l)], x1, bias=P[("b_proj", l)], resid=x)
+            xn2, mu2, r2 = e(T, h), e(T, dt=F32), e(T, dt=F32)
+            ops.layernorm_fwd(x1, P[("ln2_g", l)], P[("ln2_b", l)], xn2, mu2, r2, spec.ln_eps)
+            u, g = e(T, 4 * h), e(T, 4 * h)
+            ops.gemm(xn2, P[("w_fc1", l)], g, epilogue=ops.EPI_BF16_GELU, bias=P[("b_fc1", l)], aux=u)
+            x2 = e(T, h)
+            ops.gemm(g, P[("w_fc2", l)], x2, bias=P[("b_fc2", l)], resid=x1)
+            layers.append({"x": x, "xn1": xn1, "mu1": mu1, "r1": r1, "qkv": qkv, "o": o, "lse": lse,
+                           "x1": x1, "xn2": xn2, "mu2": mu2, "r2": r2, "u": u, "g": g})
+            x = x2
+        stash = {"layers": layers}
+        if s == self.S - 1:
+            xf, muf, rf = e(T, h), e(T, dt=F32), e(T, dt=F32)
+            ops.layernorm_fwd(x, P[("lnf_g", None)], P[("lnf_b", None)], xf, muf, rf, spec.ln_eps)
+            logits = e(T, spec.vocab)
+            ops.gemm(xf, P[("w_lm", None)], logits)
+            ops.xent(logits, self._labels[m], self.loss_sum, self._grad_scale)
+            stash.update(xlast=x, xf=xf, muf=muf, rf=rf, dlogits=logits)
+        elif self._dev_of(s + 1) == self.p:
+            self._local_act[(s + 1, m)] = x
+        else:
+            self._send("act", x, self._dev_of(s + 1))
+        self._stash[(s, m)] = stash
+
+    def _backward_input(self, s: int, m: int) -> None:
+        spec = self.spec
+        st = self.stages[s]
+        self._use_params(st)
+        self._touch_grads(st)
+        T, h, H, dh = spec.tokens_per_microbatch, spec.hidden, spec.heads, spec.head_dim
+        b, sl = spec.microbatch_samples, spec.seq_len
+        P, G = st.p, st.g
+        e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
+        stash = self._stash[(s, m)]
+        if s == self.S - 1:
+            dxf = e(T, h)
+            ops.gemm(stash["dlogits"], P[("w_lm", None)], dxf, b_t=True)
+            dx = e(T, h)
+            ops.layernorm_bwd(dxf, stash["xlast"], stash["muf"], stash["rf"], P[("lnf_g", None)], dx,
+                              G[("lnf_g", None)], G[("lnf_b", None)], self.ln_ws)
+            del stash["xlast"], stash["muf"], stash["rf"]
+        elif self._dev_of(s + 1) == self.p:
+            dx = self._local_grad.pop((s, m))
+        else:
+            dx = self._recv("grad", (T, h), self._dev_of(s + 1))
+        lo, hi = st.lay.layers
+        for i, l in reversed(list(enumerate(range(lo, hi)))):
+            a = stash["layers"][i]
+            d2 = dx
+            du = e(T, 4 * h)
+            ops.gemm(d2, P[("w_fc2", l)], du, b_t=True, epilogue=ops.EPI_BF16_DGELU, aux=a["u"])
+            dxn2 = e(T, h)
+            ops.gemm(du, P[("w_fc1", l)], dxn2, b_t=True)
+            dx1 = e(T, h)
+            ops.layernorm_bwd(dxn2, a["x1"], a["mu2"], a["r2"], P[("ln2_g", l)], dx1, G[("ln2_g", l)],
+                              G[("ln2_b", l)], self.ln_ws, dresid=d2)
+            do = e(T, h)
+            ops.gemm(dx1, P[("w_proj", l)], do, b_t=True)
+            dqkv = e(T, 3 * h)
+            ops.attn_bwd(a["qkv"], a["o"], a["lse"], do, dqkv, self.attn_ws, b, sl, H, dh)
+            dxn1 = e(T, h)
+            ops.gemm(dqkv, P[("w_qkv", l)], dxn1, b_t=True)
+            dxl = e(T, h)
+            ops.layernorm_bwd(dxn1, a["x"], a["mu1"], a["r1"], P[("ln1_g", l)], dxl, G[("ln1_g", l)],
+                              G[("ln1_b", l)], self.ln_ws, dresid=dx1)
+            # keep only what W needs: inputs of the linears and their output grads
+            stash["layers"][i] = {"xn1": a["xn1"], "o": a["o"], "xn2": a["xn2"], "g": a["g"],
+                                  "d2": d2, "du": du, "dx1": dx1, "dqkv": dqkv}
+            dx = dxl
+        if s == 0:
+            stash["demb"] = dx
+        elif self._dev_of(s - 1) == self.p:
+            self._local_grad[(s - 1, m)] = dx
+        else:
+            self._send("grad", dx, self._dev_of(s - 1))
+
+    def _backward_weight(self, s: int, m: int) -> None:
+        st = self.stages[s]
+        self._touch_grads(st)
+        G = st.g
+        stash = self._stash.pop((s, m))
+        lo, hi = st.lay.layers
+        for i, l in enumerate(range(lo, hi)):
+            a = stash["layers"][i]
+            for dy, x, w, bias in (("d2", "g", "w_fc2", "b_fc2"), ("du", "xn2", "w_fc1", "b_fc1"),
+                                   ("dx1", "o", "w_proj", "b_proj"), ("dqkv", "xn1", "w_qkv", "b_qkv")):
+                ops.gemm(a[dy], a[x], G[(w, l)], a_t=True, b_t=True, epilogue=ops.EPI_F32_ACC)
+                ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws)
+        if s == self.S - 1:
+            ops.gemm(stash["dlogits"], stash["xf"], G[("w_lm", None)], a_t=True, b_t=True,
+                     epilogue=ops.EPI_F32_ACC)
+        if s == 0:
+            ops.embed_bwd(self._ids[m], stash["demb"], G[("wte", None)], G[("wpe", None)],
+                          self.spec.seq_len)
+
+
+def execute(sched: Schedule, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
+            runtime: Runtime, ids: torch.Tensor, labels: torch.Tensor) -> StepResult:
+    """Run one ZeroPP training step of ``sched`` on this rank (the engine's
+    ``simulate``, `simulation.py:90`).  Returns a timed :class:`StepResult`."""
+    if sched is not runtime.sched:
+        raise ValueError("runtime was built for a different schedule")
+    t0 = time.perf_counter()
+    res = runtime.step(ids, labels)
+    res = runtime.finish_timing(res)
+    res.host_s = time.perf_counter() - t0
+    return res

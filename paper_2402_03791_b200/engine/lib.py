@@ -40,6 +40,7 @@ _SIGS = {
     "zpp_adamw": (c_int, [P, P, P, P, P, c_size, c_float, c_float, c_float, c_float, c_float, c_int,
                           c_stream]),
     "zpp_init_param": (c_int, [P, P, c_size, c_ulonglong, c_size, c_float, c_float, c_stream]),
+    "zpp_zero": (c_int, [P, c_size, c_stream]),
     "zpp_nccl_load": (c_int, [c_char_p]),
     "zpp_nccl_unique_id": (c_int, [c_char_p]),
     "zpp_comm_init": (c_int, [c_char_p, c_int, c_int, POINTER(c_void_p)]),

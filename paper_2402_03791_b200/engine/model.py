@@ -1,0 +1,175 @@
+"""GPT model description and the flat, ZeRO-shardable parameter layout of a stage.
+
+The reference models a stage only as ``layers * M_w`` bytes (ModelSpec,
+`config.py:36-89`; stage bytes `schedules.py:45-49`).  The engine needs the
+real tensors: a GPT-2 style pre-LN decoder (untied LM head, tanh GeLU,
+causal attention) whose parameters for each pipeline stage live in ONE flat
+bf16 buffer, so that a stage's ZeRO-3 all-gather / reduce-scatter is a single
+NCCL call on a contiguous range (AG_PARAM / RS_GRAD, `schedules.py:72-78`).
+
+Layout of stage s with layers [lo, hi) (each tensor 64-element aligned):
+    s == 0   : wte [V, h], wpe [S, h]
+    per layer: ln1_g, ln1_b, w_qkv [3h, h], b_qkv, w_proj [h, h], b_proj,
+               ln2_g, ln2_b, w_fc1 [4h, h], b_fc1, w_fc2 [h, 4h], b_fc2
+    s == S-1 : lnf_g, lnf_b, w_lm [V, h]
+The flat size is padded to a multiple of 64*D so every ZeRO shard is 128-byte
+aligned.  Shard z of D owns elements [z*n/D, (z+1)*n/D).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+ALIGN = 64
+
+LAYER_TENSORS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_proj", "b_proj",
+                 "ln2_g", "ln2_b", "w_fc1", "b_fc1", "w_fc2", "b_fc2")
+
+
+@dataclass(frozen=True)
+class GPTSpec:
+    """Engine-side model + optimizer settings (the reference config has no such
+    section, SURVEY.md section 5 'config / flag system')."""
+
+    num_layers: int
+    hidden: int
+    heads: int
+    seq_len: int
+    vocab: int = 50304
+    microbatch_samples: int = 1
+    ln_eps: float = 1e-5
+    init_std: float = 0.02
+    seed: int = 20240817
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.95
+    adam_eps: float = 1e-8
+    weight_decay: float = 0.1
+
+    def __post_init__(self):
+        if self.hidden % self.heads:
+            raise ValueError("hidden must be divisible by heads")
+        if self.head_dim not in (64, 128):
+            raise ValueError("head_dim must be 64 or 128 (attention kernels)")
+        if self.seq_len % 64 or self.hidden % 64 or self.vocab % 64:
+            raise ValueError("seq_len, hidden and vocab must be multiples of 64")
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+    @property
+    def ffn(self) -> int:
+        return 4 * self.hidden
+
+    @property
+    def tokens_per_microbatch(self) -> int:
+        return self.microbatch_samples * self.seq_len
+
+    def flops_per_token(self) -> float:
+        """Model FLOPs per token (fwd+bwd, attention at full s^2)."""
+        L, h, s, V = self.num_layers, self.hidden, self.seq_len, self.vocab
+        return 72.0 * L * h * h + 12.0 * L * s * h + 6.0 * h * V
+
+    def num_params(self) -> int:
+        h, L, V, S = self.hidden, self.num_layers, self.vocab, self.seq_len
+        per_layer = 12 * h * h + 13 * h
+        return L * per_layer + V * h + S * h + 2 * h + V * h
+
+    @classmethod
+    def gpt_6p2b(cls, **kw) -> "GPTSpec":
+        return cls(num_layers=32, hidden=4096, heads=32, seq_len=2048, **kw)
+
+    @classmethod
+    def gpt_1p3b(cls, **kw) -> "GPTSpec":
+        return cls(num_layers=24, hidden=2048, heads=16, seq_len=2048, **kw)
+
+    @classmethod
+    def tiny(cls, **kw) -> "GPTSpec":
+        return cls(num_layers=4, hidden=256, heads=4, seq_len=128, **kw)
+
+
+@dataclass(frozen=True)
+class TensorSlot:
+    name: str
+    layer: int | None          # global layer index (None for embedding / head)
+    shape: tuple[int, ...]
+    offset: int                # element offset in the flat stage buffer
+    uid: int                   # global tensor id, seeds the initialiser
+    mean: float
+    std: float
+
+    @property
+    def numel(self) -> int:
+        return math.prod(self.shape)
+
+
+def _align(n: int, a: int = ALIGN) -> int:
+    return (n + a - 1) // a * a
+
+
+@dataclass
+class StageLayout:
+    stage: int
+    layers: tuple[int, int]
+    slots: list[TensorSlot] = field(default_factory=list)
+    numel: int = 0          # padded flat size
+    shard_numel: int = 0
+
+    def slot(self, name: str, layer: int | None = None) -> TensorSlot:
+        for s in self.slots:
+            if s.name == name and s.layer == layer:
+                return s
+        raise KeyError((name, layer))
+
+
+def stage_layout(spec: GPTSpec, stage: int, num_stages: int, layer_range: tuple[int, int],
+                 dp: int) -> StageLayout:
+    h, V, L = spec.hidden, spec.vocab, spec.num_layers
+    std, proj_std = spec.init_std, spec.init_std / math.sqrt(2.0 * L)
+    lay = StageLayout(stage, layer_range)
+    off = 0
+
+    def add(name, layer, shape, uid, mean=0.0, sd=0.0):
+        nonlocal off
+        slot = TensorSlot(name, layer, tuple(shape), off, uid, mean, sd)
+        lay.slots.append(slot)
+        off = _align(off + slot.numel)
+
+    if stage == 0:
+        add("wte", None, (V, h), 1, sd=std)
+        add("wpe", None, (spec.seq_len, h), 2, sd=std)
+    for l in range(*layer_range):
+        base = 16 + 16 * l
+        shapes = {"ln1_g": (h,), "ln1_b": (h,), "w_qkv": (3 * h, h), "b_qkv": (3 * h,),
+                  "w_proj": (h, h), "b_proj": (h,), "ln2_g": (h,), "ln2_b": (h,),
+                  "w_fc1": (4 * h, h), "b_fc1": (4 * h,), "w_fc2": (h, 4 * h), "b_fc2": (h,)}
+        for j, name in enumerate(LAYER_TENSORS):
+            if name.endswith("_g"):
+                add(name, l, shapes[name], base + j, mean=1.0)
+            elif name.startswith("w_"):
+                add(name, l, shapes[name], base + j, sd=proj_std if name in ("w_proj", "w_fc2") else std)
+            else:
+                add(name, l, shapes[name], base + j)
+    if stage == num_stages - 1:
+        add("lnf_g", None, (h,), 3, mean=1.0)
+        add("lnf_b", None, (h,), 4)
+        add("w_lm", None, (V, h), 5, sd=std)
+    lay.numel = _align(off, ALIGN * dp)
+    lay.shard_numel = lay.numel // dp
+    return lay
+
+
+def init_offset(uid: int) -> int:
+    """Counter base of a tensor for the deterministic initialiser (2^40 per tensor)."""
+    return uid << 40
+
+
+def shard_init_ranges(lay: StageLayout, z: int):
+    """(slot, start_in_tensor, start_in_shard, count) for every tensor piece in shard z."""
+    lo, hi = z * lay.shard_numel, (z + 1) * lay.shard_numel
+    for slot in lay.slots:
+        a, b = max(lo, slot.offset), min(hi, slot.offset + slot.numel)
+        if a < b:
+            yield slot, a - slot.offset, a - lo, b - a

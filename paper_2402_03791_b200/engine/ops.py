@@ -116,3 +116,8 @@ def adamw(master, m, v, grad, param_bf16, lr, beta1, beta2, eps, wd, step, strea
 def init_param(master, param_bf16, seed, offset, mean, std, stream=None):
     lib.call("zpp_init_param", _p(master), _p(param_bf16), master.numel(), seed, offset, mean, std,
              _s(stream))
+
+
+def zero(t, stream=None):
+    """cudaMemsetAsync(0) of a whole tensor on ``stream`` (no torch fill kernel)."""
+    lib.call("zpp_zero", _p(t), t.numel() * t.element_size(), _s(stream))

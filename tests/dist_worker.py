@@ -1,0 +1,52 @@
+"""One rank of a multi-GPU ZeroPP step under torchrun; compares its shards with the oracle.
+
+usage: torchrun --nproc-per-node P*D dist_worker.py P D B U V OUTDIR
+"""
+
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+from engine_harness import LOSS_RTOL, compare_shards, oracle_for, run_engine_step  # noqa: E402
+from paper_2402_03791_b200.engine import GPTSpec  # noqa: E402
+
+
+def main():
+    P, D, B, U, V = (int(x) for x in sys.argv[1:6])
+    out = sys.argv[6]
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("gloo")
+    spec = GPTSpec.tiny()
+    msg = "OK"
+    try:
+        rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, P, D, B, U, V, rank=rank, world=world)
+        loss_sum = torch.tensor([res[0].loss_sum.item()])
+        dist.all_reduce(loss_sum)
+        loss = loss_sum.item() / (D * B * spec.tokens_per_microbatch)
+        loss_o, grads_o, new_o = oracle_for(spec, cfg, pl, tokens[0])
+        fails = compare_shards(spec, cfg, pl, rt, grads_o, new_o)
+        if abs(loss - loss_o) / loss_o > LOSS_RTOL:
+            fails.append(f"loss {loss} vs oracle {loss_o}")
+        if fails:
+            msg = "FAIL " + "; ".join(fails)
+        else:
+            msg = f"OK loss={loss:.5f} oracle={loss_o:.5f} step_ms={res[0].step_ms:.2f}"
+    except Exception as exc:  # report, then fail the rank
+        import traceback
+        msg = "FAIL " + traceback.format_exc()
+    with open(os.path.join(out, f"rank{rank}.txt"), "w") as f:
+        f.write(msg)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if msg.startswith("OK") else 1)
+
+
+if __name__ == "__main__":
+    main()
