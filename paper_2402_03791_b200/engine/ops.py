@@ -12,6 +12,37 @@ from . import lib
 from .lib import EPI_BF16, EPI_BF16_DGELU, EPI_BF16_GELU, EPI_F32, EPI_F32_ACC  # noqa: F401
 
 
+class _Profile:
+    """Counts libzpp kernel launches and times every GEMM launch with CUDA events
+    on its own stream (bench.py's live roofline, 'gpu_launches')."""
+
+    def __init__(self):
+        self.active = False
+        self.launches = 0
+        self._gemms: list = []
+
+    def start(self) -> None:
+        self.active, self.launches, self._gemms = True, 0, []
+
+    def stop(self):
+        """-> (total GEMM FLOPs, summed GEMM launch ms, GEMM launches); synchronizes."""
+        torch.cuda.synchronize()
+        self.active = False
+        flops = sum(f for f, _, _ in self._gemms)
+        ms = sum(a.elapsed_time(b) for _, a, b in self._gemms)
+        n = len(self._gemms)
+        self._gemms = []
+        return flops, ms, n
+
+
+PROFILE = _Profile()
+
+
+def _count(n: int) -> None:
+    if PROFILE.active:
+        PROFILE.launches += n
+
+
 def _s(stream) -> int:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -36,14 +67,25 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_t: bool = False
     N = b.shape[1] if b_t else b.shape[0]
     assert (b.shape[0] if b_t else b.shape[1]) == K, "inner dimensions differ"
     assert c.shape[0] == M and c.shape[1] == N
+    sid = _s(stream)
+    if PROFILE.active:
+        ts = torch.cuda.ExternalStream(sid)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(ts)
     lib.call("zpp_gemm", _p(a), int(a_t), _ld(a), _p(b), int(b_t), _ld(b), _p(c), _ld(c), M, N, K,
              epilogue, _p(bias), _p(resid), _ld(resid) if resid is not None else 0,
-             _p(aux), _ld(aux) if aux is not None else 0, _s(stream))
+             _p(aux), _ld(aux) if aux is not None else 0, sid)
+    if PROFILE.active:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(ts)
+        PROFILE.launches += 1
+        PROFILE._gemms.append((2.0 * M * N * K, e0, e1))
     return c
 
 
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
+    _count(1)
     lib.call("zpp_layernorm_fwd", _p(x), _p(gamma), _p(beta), _p(y), _p(mean), _p(rstd), rows, cols,
              eps, _s(stream))
 
@@ -54,12 +96,14 @@ def layernorm_bwd_workspace(rows: int, cols: int) -> int:
 
 def layernorm_bwd(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, workspace, dresid=None, stream=None):
     rows, cols = x.shape
+    _count(2)
     lib.call("zpp_layernorm_bwd", _p(dy), _p(x), _p(mean), _p(rstd), _p(gamma), _p(dresid), _p(dx),
              _p(dgamma), _p(dbeta), _p(workspace), rows, cols, _s(stream))
 
 
 def colsum_acc(dy, dbias, workspace, stream=None):
     rows, cols = dy.shape
+    _count(2)
     lib.call("zpp_colsum_acc", _p(dy), _ld(dy), _p(dbias), _p(workspace), rows, cols, _s(stream))
 
 
@@ -68,10 +112,12 @@ def colsum_workspace(rows: int, cols: int) -> int:
 
 
 def gelu(u, g, stream=None):
+    _count(1)
     lib.call("zpp_gelu_fwd", _p(u), _p(g), u.numel(), _s(stream))
 
 
 def attn_fwd(qkv, out, lse, batch, seq, heads, head_dim, stream=None):
+    _count(1)
     lib.call("zpp_attn_fwd", _p(qkv), _p(out), _p(lse), batch, seq, heads, head_dim, _s(stream))
 
 
@@ -80,40 +126,48 @@ def attn_bwd_workspace(batch, seq, heads, head_dim) -> int:
 
 
 def attn_bwd(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, head_dim, stream=None):
+    _count(3)
     lib.call("zpp_attn_bwd", _p(qkv), _p(out), _p(lse), _p(dout), _p(dqkv), _p(workspace), batch, seq,
              heads, head_dim, _s(stream))
 
 
 def embed_fwd(ids, wte, wpe, out, seq, stream=None):
     tokens, hidden = out.shape
+    _count(1)
     lib.call("zpp_embed_fwd", _p(ids), _p(wte), _p(wpe), _p(out), tokens, seq, hidden, _s(stream))
 
 
 def embed_bwd(ids, dout, dwte, dwpe, seq, stream=None):
     tokens, hidden = dout.shape
+    _count(1)
     lib.call("zpp_embed_bwd", _p(ids), _p(dout), _p(dwte), _p(dwpe), tokens, seq, hidden, _s(stream))
 
 
 def xent(logits, labels, loss_sum, grad_scale, stream=None):
     rows, vocab = logits.shape
+    _count(1)
     lib.call("zpp_xent_fwd_bwd", _p(logits), _ld(logits), _p(labels), _p(loss_sum), rows, vocab,
              grad_scale, _s(stream))
 
 
 def cast_scale(src_f32, dst_bf16, scale=1.0, stream=None):
+    _count(1)
     lib.call("zpp_cast_scale_f32_bf16", _p(src_f32), _p(dst_bf16), src_f32.numel(), scale, _s(stream))
 
 
 def accum(src_bf16, acc_f32, stream=None):
+    _count(1)
     lib.call("zpp_accum_bf16_f32", _p(src_bf16), _p(acc_f32), src_bf16.numel(), _s(stream))
 
 
 def adamw(master, m, v, grad, param_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
+    _count(1)
     lib.call("zpp_adamw", _p(master), _p(m), _p(v), _p(grad), _p(param_bf16), master.numel(), lr, beta1,
              beta2, eps, wd, step, _s(stream))
 
 
 def init_param(master, param_bf16, seed, offset, mean, std, stream=None):
+    _count(1)
     lib.call("zpp_init_param", _p(master), _p(param_bf16), master.numel(), seed, offset, mean, std,
              _s(stream))
 
