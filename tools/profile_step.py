@@ -1,0 +1,53 @@
+"""Kernel-time breakdown of one GPT-6.2B-width ZeroPP step (torch.profiler / CUPTI).
+
+    python tools/profile_step.py [--layers L] [--B 8] [--U 2] [--ncu]
+
+With --ncu the step is bracketed by cudaProfilerStart/Stop so that
+`ncu --profile-from-start off` captures exactly one step.
+"""
+import argparse, os, sys, collections
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from oracle.gpt_oracle import make_tokens
+from paper_2402_03791_b200 import ModelSpec, ParallelConfig, generate, make_placement
+from paper_2402_03791_b200.engine import GPTSpec, Runtime
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--layers", type=int, default=32)
+ap.add_argument("--B", type=int, default=8)
+ap.add_argument("--U", type=int, default=2)
+ap.add_argument("--ncu", action="store_true")
+a = ap.parse_args()
+spec = GPTSpec(num_layers=a.layers, hidden=4096, heads=32, seq_len=2048)
+model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
+cfg = ParallelConfig(pp_size=1, dp_size=1, microbatches=a.B, unit_size=a.U)
+pl = make_placement(cfg, model)
+sched = generate(model, cfg, pl)
+rt = Runtime(spec, model, cfg, pl, sched)
+t = make_tokens(1, 1, a.B, 1, spec.seq_len, spec.vocab)[0, 0]
+ids = t[:, :, :-1].reshape(a.B, -1).contiguous().cuda()
+lab = t[:, :, 1:].reshape(a.B, -1).contiguous().cuda()
+for _ in range(2):
+    rt.step(ids, lab)
+torch.cuda.synchronize()
+if a.ncu:
+    torch.cuda.profiler.start()
+    rt.step(ids, lab)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    sys.exit(0)
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    rt.step(ids, lab)
+    torch.cuda.synchronize()
+tot = collections.Counter(); cnt = collections.Counter()
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        name = e.name.split("(")[0].split("<")[0].replace("void ", "").replace("zpp::", "")
+        tot[name] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+        cnt[name] += 1
+all_us = sum(tot.values())
+print(f"{'kernel':40s} {'calls':>6s} {'ms':>9s} {'share':>6s}")
+for k, v in tot.most_common():
+    print(f"{k[:40]:40s} {cnt[k]:6d} {v/1e3:9.2f} {100*v/all_us:5.1f}%")
+print(f"total kernel time {all_us/1e3:.1f} ms")
