@@ -51,6 +51,10 @@ int zpp_gemm(const void* A, int a_mn_major, long long lda, const void* B, int b_
              void* C, long long ldc, int M, int N, int K, int epilogue, const void* bias, const void* resid,
              long long ldr, void* aux, long long ldaux, uintptr_t stream);
 
+/* CTA-group policy for zpp_gemm: 0 = auto (CTA pairs, cta_group::2, when M > 256),
+ * 1 = single-CTA tiles only, 2 = prefer pairs.  Process-wide. */
+int zpp_gemm_set_cta_group(int cg);
+
 /* ---- causal multi-head attention, qkv packed [b, s, 3, heads, d] bf16 --------- */
 int zpp_attn_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, int head_dim,
                  uintptr_t stream);

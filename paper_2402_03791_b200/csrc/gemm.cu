@@ -4,18 +4,25 @@
 //
 // A is K-major (A[m*lda+k]) or M-major (A[k*lda+m]); B is K-major (B[n*ldb+k]) or
 // N-major (B[k*ldb+n]).  This covers the three GEMMs of a transformer linear
-// (SURVEY.md section 2 kernel table):
+// (SURVEY.md section 2 kernel table) without any transpose pass:
 //   fwd    Y  = X  W^T   A=X  (K-major)  B=W (K-major)
 //   dgrad  dX = dY W     A=dY (K-major)  B=W (N-major)
-//   wgrad  dW += dY^T X  A=dY (M-major)  B=X (N-major), fp32 accumulate epilogue
+//   wgrad  dW += dY^T X  A=dY (M-major)  B=X (N-major), fp32 TMA reduce-add epilogue
 //
-// CTA layout (256 threads, 1 CTA/SM, persistent over output tiles):
+// CG = 1: one CTA computes a 128 x BN tile with tcgen05.mma.cta_group::1.
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
+//         tcgen05.mma.cta_group::2: each CTA TMA-loads its 128 rows of A and half of
+//         B; the leader issues the MMA and multicast-commits to both CTAs; each CTA
+//         owns the TMEM accumulator of its 128 rows.  Per-SM operand traffic drops
+//         from (128+BN)*64*2 to (128+BN/2)*64*2 bytes per k-block.
+//
+// Warp roles (256 threads, 1 CTA/SM, persistent over output tiles):
 //   warp 0     TMA producer (one lane): A/B tiles -> smem ring (128B swizzle)
-//   warp 1     MMA issuer (one lane): tcgen05.mma 128xBNx16 into TMEM
-//   warp 2     TMEM allocator
-//   warps 4-7  epilogue: tcgen05.ld -> bias/GeLU/residual/cast -> global
-// TMEM holds two BN-column fp32 accumulators so the epilogue of tile i overlaps
-// the MMAs of tile i+1.
+//   warp 1     MMA issuer (one lane, leader CTA only)
+//   warp 2     TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4-7  epilogue: tcgen05.ld -> bias/GeLU/dGeLU/residual/cast -> swizzled
+//              per-warp smem staging -> TMA store (bf16/fp32) or TMA reduce-add
+//              (fp32 +=, so the gradient accumulation never round-trips the SM).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -26,13 +33,12 @@
 
 namespace zpp {
 
-constexpr int GEMM_BM = 128;
+constexpr int GEMM_BM = 128;  // rows per CTA
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 256;
+constexpr int EPI_BUF = 4096;  // per-warp staging buffer: 32 rows x 128 B
 
 struct EpiParams {
-  void* C;
-  long long ldc;
   const __nv_bfloat16* bias;
   const __nv_bfloat16* resid;
   long long ldr;
@@ -42,46 +48,22 @@ struct EpiParams {
   int M, N;
 };
 
-template <int BN>
+template <int BN, int CG>
 struct GemmCfg {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
-  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;  // 4 epilogue warps x 2 buffers
+  static constexpr int STAGES = (224 * 1024 - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-__device__ __forceinline__ void store_row_chunk(const EpiParams& p, int row, int col, const uint32_t (&v)[32]) {
+// Epilogue math for 32 consecutive columns of one row (values in x, in place).
+__device__ __forceinline__ void epi_math(const EpiParams& p, int row, int col, float (&x)[32]) {
   const int mode = p.mode & 0xF;
   const bool full = (col + 32 <= p.N);
-  if (mode == ZPP_EPI_F32 || mode == ZPP_EPI_F32_ACC) {
-    float* c = reinterpret_cast<float*>(p.C) + (long long)row * p.ldc + col;
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 o = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                               __uint_as_float(v[j + 3]));
-        if (mode == ZPP_EPI_F32_ACC) {
-          float4 old = *reinterpret_cast<float4*>(c + j);
-          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-        }
-        *reinterpret_cast<float4*>(c + j) = o;
-      }
-    } else {
-      #pragma unroll
-      for (int j = 0; j < 32; ++j) if (col + j < p.N) {
-        float o = __uint_as_float(v[j]);
-        if (mode == ZPP_EPI_F32_ACC) o += c[j];
-        c[j] = o;
-      }
-    }
-    return;
-  }
-  // bf16 outputs
-  float x[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(v[j]);
   if (p.bias) {
     if (full) {
 #pragma unroll
@@ -91,29 +73,29 @@ __device__ __forceinline__ void store_row_chunk(const EpiParams& p, int row, int
         x[j + 4] += bf16lo(b.z); x[j + 5] += bf16hi(b.z); x[j + 6] += bf16lo(b.w); x[j + 7] += bf16hi(b.w);
       }
     } else {
-      #pragma unroll
-      for (int j = 0; j < 32; ++j) if (col + j < p.N) x[j] += __bfloat162float(p.bias[col + j]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < p.N) x[j] += __bfloat162float(p.bias[col + j]);
     }
   }
   if (mode == ZPP_EPI_BF16_GELU) {
-    if (p.aux) {
+    if (p.aux && row < p.M) {
       __nv_bfloat16* a = p.aux + (long long)row * p.ldaux + col;
       if (full) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 o = make_uint4(pack_bf16(x[j], x[j + 1]), pack_bf16(x[j + 2], x[j + 3]),
-                               pack_bf16(x[j + 4], x[j + 5]), pack_bf16(x[j + 6], x[j + 7]));
-          *reinterpret_cast<uint4*>(a + j) = o;
-        }
+        for (int j = 0; j < 32; j += 8)
+          *reinterpret_cast<uint4*>(a + j) = make_uint4(pack_bf16(x[j], x[j + 1]), pack_bf16(x[j + 2], x[j + 3]),
+                                                        pack_bf16(x[j + 4], x[j + 5]), pack_bf16(x[j + 6], x[j + 7]));
       } else {
-        #pragma unroll
-      for (int j = 0; j < 32; ++j) if (col + j < p.N) a[j] = __float2bfloat16(x[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col + j < p.N) a[j] = __float2bfloat16(x[j]);
       }
     }
     // GeLU of the bf16-rounded pre-activation, matching what backward will see
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = gelu_f(__bfloat162float(__float2bfloat16(x[j])));
-  } else if (mode == ZPP_EPI_BF16_DGELU) {
+  } else if (mode == ZPP_EPI_BF16_DGELU && row < p.M) {
     const __nv_bfloat16* a = p.aux + (long long)row * p.ldaux + col;
     if (full) {
 #pragma unroll
@@ -125,11 +107,12 @@ __device__ __forceinline__ void store_row_chunk(const EpiParams& p, int row, int
         x[j + 6] *= gelu_grad_f(bf16lo(u.w)); x[j + 7] *= gelu_grad_f(bf16hi(u.w));
       }
     } else {
-      #pragma unroll
-      for (int j = 0; j < 32; ++j) if (col + j < p.N) x[j] *= gelu_grad_f(__bfloat162float(a[j]));
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < p.N) x[j] *= gelu_grad_f(__bfloat162float(a[j]));
     }
   }
-  if (p.resid) {
+  if (p.resid && row < p.M) {
     const __nv_bfloat16* r = p.resid + (long long)row * p.ldr + col;
     if (full) {
 #pragma unroll
@@ -139,38 +122,30 @@ __device__ __forceinline__ void store_row_chunk(const EpiParams& p, int row, int
         x[j + 4] += bf16lo(b.z); x[j + 5] += bf16hi(b.z); x[j + 6] += bf16lo(b.w); x[j + 7] += bf16hi(b.w);
       }
     } else {
-      #pragma unroll
-      for (int j = 0; j < 32; ++j) if (col + j < p.N) x[j] += __bfloat162float(r[j]);
-    }
-  }
-  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc + col;
-  if (full) {
 #pragma unroll
-    for (int j = 0; j < 32; j += 8) {
-      uint4 o = make_uint4(pack_bf16(x[j], x[j + 1]), pack_bf16(x[j + 2], x[j + 3]), pack_bf16(x[j + 4], x[j + 5]),
-                           pack_bf16(x[j + 6], x[j + 7]));
-      *reinterpret_cast<uint4*>(c + j) = o;
+      for (int j = 0; j < 32; ++j)
+        if (col + j < p.N) x[j] += __bfloat162float(r[j]);
     }
-  } else {
-    #pragma unroll
-      for (int j = 0; j < 32; ++j) if (col + j < p.N) c[j] = __float2bfloat16(x[j]);
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        int M, int N, int K, EpiParams ep) {
-  using Cfg = GemmCfg<BN>;
+                        const __grid_constant__ CUtensorMap tmC, int M, int N, int K, EpiParams ep) {
+  using Cfg = GemmCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int TILE_M = GEMM_BM * CG;
+  constexpr int BNL = BN / CG;  // B rows (N) loaded by this CTA
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sA = base;                                   // STAGES * A_BYTES
-  const uint32_t sB = base + STAGES * Cfg::A_BYTES;           // STAGES * B_BYTES
-  const uint32_t bars = base + STAGES * Cfg::STAGE_BYTES;     // barrier block
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * Cfg::STAGE_BYTES + 200);
+  const uint32_t sA = base;
+  const uint32_t sB = base + STAGES * Cfg::A_BYTES;
+  const uint32_t sE = base + STAGES * Cfg::STAGE_BYTES;  // epilogue staging (1024-aligned)
+  const uint32_t bars = sE + Cfg::EPI_BYTES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 200);
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
@@ -178,58 +153,71 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = (CG == 2) ? cluster_rank() : 0u;
+  const bool leader = crank == 0;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
+      // One arrival (the leader's expect_tx); the peer's TMA bytes complete the
+      // transaction on the leader's barrier.  (A .release.cluster remote arrive per
+      // stage here halved pair throughput: it compiles to MEMBAR+ERRBAR.)
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 128);
+      mbar_init(tempty_bar(a), 128 * CG);  // every epilogue thread of the pair
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if (CG == 2) tmem_alloc2(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    else tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
+  const int num_m = (M + TILE_M - 1) / TILE_M;
   const int num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_k = (K + GEMM_BK - 1) / GEMM_BK;
+  const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % num_m) * GEMM_BM;
-        const int n0 = (tile / num_m) * BN;
+      for (int tile = unit; tile < num_tiles; tile += nunits) {
+        const int m0 = (tile % num_m) * TILE_M + crank * GEMM_BM;
+        const int n0 = (tile / num_m) * BN + crank * BNL;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t fb = full_bar(stage);
-          mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES * CG);
           const int k0 = kb * GEMM_BK;
           const uint32_t a_dst = sA + stage * Cfg::A_BYTES;
           const uint32_t b_dst = sB + stage * Cfg::B_BYTES;
+          auto load = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 2) tma_load_2d_2sm(dst, m, fb, c0, c1);
+            else tma_load_2d(dst, m, fb, c0, c1);
+          };
           if (!A_MN) {
-            tma_load_2d(a_dst, &tmA, fb, k0, m0);  // box {64 k, 128 m}
+            load(a_dst, &tmA, k0, m0);  // box {64 k, 128 m}
           } else {
 #pragma unroll
-            for (int i = 0; i < GEMM_BM / 64; ++i)  // boxes {64 m, 64 k}
-              tma_load_2d(a_dst + i * 64 * GEMM_BK * 2, &tmA, fb, m0 + 64 * i, k0);
+            for (int i = 0; i < GEMM_BM / 64; ++i) load(a_dst + i * 64 * GEMM_BK * 2, &tmA, m0 + 64 * i, k0);
           }
           if (!B_MN) {
-            tma_load_2d(b_dst, &tmB, fb, k0, n0);  // box {64 k, BN n}
+            load(b_dst, &tmB, k0, n0);  // box {64 k, BNL n}
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(b_dst + i * 64 * GEMM_BK * 2, &tmB, fb, n0 + 64 * i, k0);
+            for (int i = 0; i < BNL / 64; ++i) load(b_dst + i * 64 * GEMM_BK * 2, &tmB, n0 + 64 * i, k0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -237,18 +225,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
-      // K-major: SBO = 8 rows * 128 B; MN-major: LBO = stride between 64-wide MN atoms.
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(TILE_M, BN, A_MN, B_MN);
       constexpr uint32_t A_LBO = A_MN ? 64 * GEMM_BK * 2 : 16;
       constexpr uint32_t B_LBO = B_MN ? 64 * GEMM_BK * 2 : 16;
-      // advance per UMMA_K=16 step: K-major +32 B inside the swizzled row; MN-major +16 rows.
       constexpr uint32_t A_KSTEP = A_MN ? 16 * 128 : 32;
       constexpr uint32_t B_KSTEP = B_MN ? 16 * 128 : 32;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(tempty_bar(acc), acc_phase ^ 1);
@@ -263,85 +249,187 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = make_sdesc(a_s + k * A_KSTEP, A_LBO, 1024);
             const uint64_t bd = make_sdesc(b_s + k * B_KSTEP, B_LBO, 1024);
-            mma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            if (CG == 2) mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            else mma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
           }
-          mma_commit(empty_bar(stage));  // frees the smem slot once these MMAs retire
+          if (CG == 2) mma_commit_2sm(empty_bar(stage), 0x3);
+          else mma_commit(empty_bar(stage));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(tfull_bar(acc));  // accumulator ready for the epilogue
+        if (CG == 2) mma_commit_2sm(tfull_bar(acc), 0x3);
+        else mma_commit(tfull_bar(acc));
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row_in_tile = q * 32 + lane;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    const int mode = ep.mode & 0xF;
+    const bool f32out = (mode == ZPP_EPI_F32 || mode == ZPP_EPI_F32_ACC);
+    const uint32_t ebuf0 = sE + q * 2 * EPI_BUF;
+    const uint32_t tempty_leader = (CG == 2) ? map_cta(tempty_bar(0), 0) : tempty_bar(0);
+    int it = 0, nb = 0;  // nb: staging buffers used so far (ring of 2)
+    for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % num_m) * GEMM_BM;
+      const int row0 = (tile % num_m) * TILE_M + crank * GEMM_BM + q * 32;
       const int n0 = (tile / num_m) * BN;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      const int row = m0 + row_in_tile;
+      const int row = row0 + lane;
+      constexpr int CHUNK = 32;
+      const int cols_per_store = f32out ? 32 : 64;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_row + c * 32, v);
-        tmem_wait_ld();
-        const int col = n0 + c * 32;
-        if (row < M && col < N) store_row_chunk(ep, row, col, v);
+      for (int c = 0; c < BN; c += cols_per_store) {
+        float x[2][32];
+        const int nsub = cols_per_store / CHUNK;
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          if (sub < nsub) {
+            uint32_t v[32];
+            tmem_ld32(t_row + c + sub * CHUNK, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[sub][j] = __uint_as_float(v[j]);
+          }
+        }
+        if (c + cols_per_store >= BN) {  // accumulator fully in registers: release TMEM early
+          tc_fence_before();
+          if (CG == 2) mbar_arrive_remote(tempty_leader + 8u * acc);
+          else mbar_arrive(tempty_bar(acc));
+        }
+        const int col = n0 + c;
+        if (col >= N) continue;  // whole chunk beyond the matrix (ragged last tile)
+        if (!f32out) {
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub)
+            if (col + sub * CHUNK < N) epi_math(ep, row, col + sub * CHUNK, x[sub]);
+        }
+        // stage this warp's 32 rows x 128 B into a 128B-swizzled buffer, then TMA it out
+        const uint32_t buf = ebuf0 + (nb & 1) * EPI_BUF;
+        if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
+        __syncwarp();
+        const uint32_t rbase = buf + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t w0, w1, w2, w3;
+          if (f32out) {
+            w0 = __float_as_uint(x[0][4 * j]); w1 = __float_as_uint(x[0][4 * j + 1]);
+            w2 = __float_as_uint(x[0][4 * j + 2]); w3 = __float_as_uint(x[0][4 * j + 3]);
+          } else {
+            const float* s = &x[j >> 2][(j & 3) * 8];
+            w0 = pack_bf16(s[0], s[1]); w1 = pack_bf16(s[2], s[3]);
+            w2 = pack_bf16(s[4], s[5]); w3 = pack_bf16(s[6], s[7]);
+          }
+          st_shared_v4(rbase + ((j ^ (lane & 7)) << 4), w0, w1, w2, w3);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if (mode == ZPP_EPI_F32_ACC) tma_reduce_add_2d(&tmC, buf, col, row0);
+          else tma_store_2d(&tmC, buf, col, row0);
+          bulk_commit();
+        }
+        ++nb;
       }
-      tc_fence_before();
-      mbar_arrive(tempty_bar(acc));
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if (CG == 2) tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // host side
 
-static int make_map_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                         uint32_t box_inner, uint32_t box_outer) {
+static int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* ptr, uint64_t inner,
+                    uint64_t outer, uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint64_t strides[1] = {ld_elems * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  return encode_tensor_map(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-                           estr, CU_TENSOR_MAP_SWIZZLE_128B);
+  return encode_tensor_map(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <int BN, bool A_MN, bool B_MN>
-static int launch_gemm(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K,
-                       const EpiParams& ep, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
-  CUtensorMap ma, mb;
+template <int BN, bool A_MN, bool B_MN, int CG>
+static int launch_gemm(const void* A, long long lda, const void* B, long long ldb, void* C, long long ldc, int M,
+                       int N, int K, const EpiParams& ep, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN, CG>;
+  constexpr int BNL = BN / CG;
+  const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUtensorMap ma, mb, mc;
   int rc;
-  if (!A_MN) rc = make_map_bf16(&ma, A, K, M, lda, GEMM_BK, GEMM_BM);
-  else rc = make_map_bf16(&ma, A, M, K, lda, 64, GEMM_BK);
+  if (!A_MN) rc = make_map(&ma, BF, 2, A, K, M, lda, GEMM_BK, GEMM_BM);
+  else rc = make_map(&ma, BF, 2, A, M, K, lda, 64, GEMM_BK);
   if (rc) return rc;
-  if (!B_MN) rc = make_map_bf16(&mb, B, K, N, ldb, GEMM_BK, BN);
-  else rc = make_map_bf16(&mb, B, N, K, ldb, 64, GEMM_BK);
+  if (!B_MN) rc = make_map(&mb, BF, 2, B, K, N, ldb, GEMM_BK, BNL);
+  else rc = make_map(&mb, BF, 2, B, N, K, ldb, 64, GEMM_BK);
   if (rc) return rc;
-  auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN>;
+  const int mode = ep.mode & 0xF;
+  if (mode == ZPP_EPI_F32 || mode == ZPP_EPI_F32_ACC)
+    rc = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, N, M, ldc, 32, 32);
+  else
+    rc = make_map(&mc, BF, 2, C, N, M, ldc, 64, 32);
+  if (rc) return rc;
+  auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_set = true;
   }
-  const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ma, mb, M, N, K, ep);
+  const int tiles = ((M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((N + BN - 1) / BN);
+  const int units = num_sms() / CG;
+  const int grid = (tiles < units ? tiles : units) * CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep);
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return check_launch("gemm_tcgen05");
 }
 
+template <bool A_MN, bool B_MN>
+static int dispatch(const void* A, long long lda, const void* B, long long ldb, void* C, long long ldc, int M, int N,
+                    int K, const EpiParams& ep, cudaStream_t s, int cg_pref) {
+  // Pairs (CG=2, 256-row tiles) whenever there are at least two 256-row tiles; narrow
+  // problems use 128-wide tiles so the last N tile wastes less.
+  const bool pair = (cg_pref != 1) && M > 256;
+  const bool wide = N > 128;
+  if (pair) {
+    return wide ? launch_gemm<256, A_MN, B_MN, 2>(A, lda, B, ldb, C, ldc, M, N, K, ep, s)
+                : launch_gemm<128, A_MN, B_MN, 2>(A, lda, B, ldb, C, ldc, M, N, K, ep, s);
+  }
+  return wide ? launch_gemm<256, A_MN, B_MN, 1>(A, lda, B, ldb, C, ldc, M, N, K, ep, s)
+              : launch_gemm<128, A_MN, B_MN, 1>(A, lda, B, ldb, C, ldc, M, N, K, ep, s);
+}
+
 }  // namespace zpp
+
+static int g_cg_pref = 0;  // 0 = auto, 1 = force single-CTA tiles, 2 = prefer pairs
+
+extern "C" int zpp_gemm_set_cta_group(int cg) {
+  if (cg < 0 || cg > 2) return zpp::set_error(ZPP_ERR_ARG, "cta group must be 0, 1 or 2");
+  g_cg_pref = cg;
+  return ZPP_OK;
+}
 
 extern "C" int zpp_gemm(const void* A, int a_mn_major, long long lda, const void* B, int b_mn_major,
                         long long ldb, void* C, long long ldc, int M, int N, int K, int epilogue,
@@ -350,27 +438,21 @@ extern "C" int zpp_gemm(const void* A, int a_mn_major, long long lda, const void
   using namespace zpp;
   if (M <= 0 || N <= 0 || K <= 0) return set_error(ZPP_ERR_ARG, "gemm: empty shape");
   if ((lda % 8) || (ldb % 8)) return set_error(ZPP_ERR_ARG, "gemm: lda/ldb must be multiples of 8 elements");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
-    return set_error(ZPP_ERR_ARG, "gemm: A/B must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return set_error(ZPP_ERR_ARG, "gemm: A/B/C must be 16-byte aligned");
   const int mode = epilogue & 0xF;
+  if (epilogue >> 4) return set_error(ZPP_ERR_ARG, "gemm: bad epilogue flags");
   if (mode > ZPP_EPI_F32_ACC) return set_error(ZPP_ERR_ARG, "gemm: bad epilogue");
   if (mode == ZPP_EPI_BF16_DGELU && !aux) return set_error(ZPP_ERR_ARG, "gemm: DGELU needs aux");
   if ((N % 8) || (ldc % 8) || (resid && ldr % 8) || (aux && ldaux % 8))
     return set_error(ZPP_ERR_ARG, "gemm: N/ldc/ldr/ldaux must be multiples of 8");
-  EpiParams ep{C, ldc, reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(resid),
-               ldr, reinterpret_cast<__nv_bfloat16*>(aux), ldaux, epilogue, M, N};
+  const bool f32 = (mode == ZPP_EPI_F32 || mode == ZPP_EPI_F32_ACC);
+  if (f32 && (bias || resid)) return set_error(ZPP_ERR_ARG, "gemm: fp32 epilogues take no bias/resid");
+  EpiParams ep{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(resid), ldr,
+               reinterpret_cast<__nv_bfloat16*>(aux), ldaux, epilogue, M, N};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // Narrow problems waste half a 256-wide tile; use BN=128 there.
-  const bool wide = N > 128;
-  if (!a_mn_major && !b_mn_major)
-    return wide ? launch_gemm<256, false, false>(A, lda, B, ldb, M, N, K, ep, s)
-                : launch_gemm<128, false, false>(A, lda, B, ldb, M, N, K, ep, s);
-  if (!a_mn_major && b_mn_major)
-    return wide ? launch_gemm<256, false, true>(A, lda, B, ldb, M, N, K, ep, s)
-                : launch_gemm<128, false, true>(A, lda, B, ldb, M, N, K, ep, s);
-  if (a_mn_major && b_mn_major)
-    return wide ? launch_gemm<256, true, true>(A, lda, B, ldb, M, N, K, ep, s)
-                : launch_gemm<128, true, true>(A, lda, B, ldb, M, N, K, ep, s);
-  return wide ? launch_gemm<256, true, false>(A, lda, B, ldb, M, N, K, ep, s)
-              : launch_gemm<128, true, false>(A, lda, B, ldb, M, N, K, ep, s);
+  if (!a_mn_major && !b_mn_major) return dispatch<false, false>(A, lda, B, ldb, C, ldc, M, N, K, ep, s, g_cg_pref);
+  if (!a_mn_major && b_mn_major) return dispatch<false, true>(A, lda, B, ldb, C, ldc, M, N, K, ep, s, g_cg_pref);
+  if (a_mn_major && b_mn_major) return dispatch<true, true>(A, lda, B, ldb, C, ldc, M, N, K, ep, s, g_cg_pref);
+  return dispatch<true, false>(A, lda, B, ldb, C, ldc, M, N, K, ep, s, g_cg_pref);
 }

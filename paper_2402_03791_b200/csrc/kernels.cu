@@ -95,115 +95,120 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
   }
 }
 
-// dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid).
-// Each block handles LN_RPB rows and writes per-block column partials of
-// dgamma = sum dy*xhat and dbeta = sum dy (reduced by ln_param_reduce_kernel).
-constexpr int LN_RPB = 8;
-
-__global__ void __launch_bounds__(256) layernorm_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                                            const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                            const bf16* __restrict__ g, const bf16* __restrict__ dres,
-                                                            bf16* __restrict__ dx, float* __restrict__ part, int rows,
-                                                            int cols) {
-  __shared__ float red[8];
+// dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
+// the two row sums fused into a single float2 block reduction.
+__global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd,
+                                                               const bf16* __restrict__ g, const bf16* __restrict__ dres,
+                                                               bf16* __restrict__ dx, int cols) {
+  __shared__ float2 red[8];
+  const int row = blockIdx.x;
   const int nvec = cols / 8;
-  float pg[LN_VPT][8], pb[LN_VPT][8], gg[LN_VPT][8];
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * 256;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) { pg[i][j] = 0.f; pb[i][j] = 0.f; gg[i][j] = 0.f; }
-    if (vi < nvec) unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg[i]);
-  }
-  for (int r = 0; r < LN_RPB; ++r) {
-    const int row = blockIdx.x * LN_RPB + r;
-    if (row >= rows) break;
-    const float mu = mean[row], rs = rstd[row];
-    const bf16* xr = x + (long long)row * cols;
-    const bf16* dyr = dy + (long long)row * cols;
-    float xh[LN_VPT][8], dg[LN_VPT][8];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * 256;
-      if (vi < nvec) {
-        float xv[8], dv[8];
-        unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), xv);
-        unpack8(*reinterpret_cast<const uint4*>(dyr + vi * 8), dv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          xh[i][j] = (xv[j] - mu) * rs;
-          dg[i][j] = dv[j] * gg[i][j];
-          s1 += dg[i][j];
-          s2 += dg[i][j] * xh[i][j];
-          pg[i][j] += dv[j] * xh[i][j];
-          pb[i][j] += dv[j];
-        }
-      }
-    }
-    const float m1 = block_sum256(s1, red) / cols;
-    const float m2 = block_sum256(s2, red) / cols;
-    bf16* dxr = dx + (long long)row * cols;
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * 256;
-      if (vi < nvec) {
-        float o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = rs * (dg[i][j] - m1 - xh[i][j] * m2);
-        if (dres) {
-          float rv[8];
-          unpack8(*reinterpret_cast<const uint4*>(dres + (long long)row * cols + vi * 8), rv);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] += rv[j];
-        }
-        *reinterpret_cast<uint4*>(dxr + vi * 8) = pack8(o);
-      }
-    }
-  }
-  float* pgo = part + (long long)blockIdx.x * 2 * cols;
-  float* pbo = pgo + cols;
+  const float mu = mean[row], rs = rstd[row];
+  const bf16* xr = x + (long long)row * cols;
+  const bf16* dyr = dy + (long long)row * cols;
+  float xh[LN_VPT][8], dg[LN_VPT][8];
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * 256;
     if (vi < nvec) {
+      float xv[8], dv[8], gv[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dyr + vi * 8), dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gv);
 #pragma unroll
-      for (int j = 0; j < 8; j += 4) {
-        *reinterpret_cast<float4*>(pgo + vi * 8 + j) = make_float4(pg[i][j], pg[i][j + 1], pg[i][j + 2], pg[i][j + 3]);
-        *reinterpret_cast<float4*>(pbo + vi * 8 + j) = make_float4(pb[i][j], pb[i][j + 1], pb[i][j + 2], pb[i][j + 3]);
+      for (int j = 0; j < 8; ++j) {
+        xh[i][j] = (xv[j] - mu) * rs;
+        dg[i][j] = dv[j] * gv[j];
+        s1 += dg[i][j];
+        s2 += dg[i][j] * xh[i][j];
       }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = make_float2(s1, s2);
+  __syncthreads();
+  float2 t = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) { t.x += red[i].x; t.y += red[i].y; }
+  const float m1 = t.x / cols, m2 = t.y / cols;
+  bf16* dxr = dx + (long long)row * cols;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * 256;
+    if (vi < nvec) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = rs * (dg[i][j] - m1 - xh[i][j] * m2);
+      if (dres) {
+        float rv[8];
+        unpack8(*reinterpret_cast<const uint4*>(dres + (long long)row * cols + vi * 8), rv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] += rv[j];
+      }
+      *reinterpret_cast<uint4*>(dxr + vi * 8) = pack8(o);
     }
   }
 }
 
-// out_k[c] += sum_b part[b][k*cols + c]  for k in [0, nout)   (fixed order)
-__global__ void partial_reduce_kernel(const float* __restrict__ part, int nblk, int width, float* out0,
-                                      float* out1, int cols) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= width) return;
-  float s = 0.f;
-  for (int b = 0; b < nblk; ++b) s += part[(long long)b * width + c];
-  if (c < cols) out0[c] += s;
-  else out1[c - cols] += s;
-}
-
-// Column sums of a bf16 [rows, cols] matrix (row stride ld): per 64-row block partials.
-constexpr int CS_RPB = 64;
-__global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16* __restrict__ y, long long ld,
-                                                             float* __restrict__ part, int rows, int cols) {
-  const int c8 = blockIdx.x * 256 + threadIdx.x;  // vector of 8 columns
-  if (c8 * 8 >= cols) return;
-  const int r0 = blockIdx.y * CS_RPB;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0; r < r0 + CS_RPB && r < rows; ++r) {
-    float v[8];
-    unpack8(*reinterpret_cast<const uint4*>(y + (long long)r * ld + c8 * 8), v);
+// Column reductions over all rows of a 32-column strip per block (deterministic, one pass):
+//   LN mode : out0[c] += sum_r dy[r,c] * (x[r,c]-mean[r])*rstd[r],  out1[c] += sum_r dy[r,c]
+//   SUM mode: out0[c] += sum_r dy[r,c]                               (bias gradients)
+// 256 threads = 4 column vectors (8 bf16) x 64 row lanes; smem tree over the row lanes.
+template <bool LN>
+__global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy, long long ld,
+                                                     const bf16* __restrict__ x, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, float* __restrict__ out0,
+                                                     float* __restrict__ out1, int rows, int cols) {
+  __shared__ float sh[LN ? 2 : 1][64][33];
+  const int cv = threadIdx.x & 3, rl = threadIdx.x >> 2;
+  const int c0 = blockIdx.x * 32 + cv * 8;
+  float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c0 < cols) {
+#pragma unroll 4
+    for (int r = rl; r < rows; r += 64) {
+      float d[8];
+      unpack8(*reinterpret_cast<const uint4*>(dy + (long long)r * ld + c0), d);
+      if (LN) {
+        float xv[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + (long long)r * cols + c0), xv);
+        const float mu = mean[r], rs = rstd[r];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += v[j];
+        for (int j = 0; j < 8; ++j) {
+          a0[j] += d[j] * (xv[j] - mu) * rs;
+          a1[j] += d[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a0[j] += d[j];
+      }
+    }
   }
-  float* o = part + (long long)blockIdx.y * cols + c8 * 8;
-  *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sh[0][rl][cv * 8 + j] = a0[j];
+    if (LN) sh[LN ? 1 : 0][rl][cv * 8 + j] = a1[j];
+  }
+  __syncthreads();
+  // 256 threads: (output k, column c) pairs, each sums 64 row-lane partials in fixed order
+  const int nout = LN ? 2 : 1;
+  for (int idx = threadIdx.x; idx < nout * 32; idx += 256) {
+    const int k = idx / 32, c = idx % 32;
+    float s = 0.f;
+    for (int r = 0; r < 64; ++r) s += sh[k][r][c];
+    const int col = blockIdx.x * 32 + c;
+    if (col < cols) {
+      if (k == 0) out0[col] += s;
+      else out1[col] += s;
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -405,37 +410,29 @@ extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* b
   return check_launch("layernorm_fwd");
 }
 
-extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) {
-  return (long long)((rows + LN_RPB - 1) / LN_RPB) * 2 * cols;
-}
+extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) { return 0; }
 
 extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                                  const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
                                  float* workspace, int rows, int cols, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: bad cols");
   if (rows <= 0) return ZPP_OK;
-  const int nblk = (rows + LN_RPB - 1) / LN_RPB;
-  layernorm_bwd_kernel<<<nblk, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
-                                                          (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx,
-                                                          workspace, rows, cols);
-  int rc = check_launch("layernorm_bwd");
+  layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
+                                                             (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
+  int rc = check_launch("layernorm_bwd_dx");
   if (rc) return rc;
-  partial_reduce_kernel<<<(2 * cols + 255) / 256, 256, 0, STREAM(stream)>>>(workspace, nblk, 2 * cols, dgamma, dbeta,
-                                                                            cols);
-  return check_launch("layernorm_bwd_reduce");
+  colred_kernel<true><<<(cols + 31) / 32, 256, 0, STREAM(stream)>>>((const bf16*)dy, cols, (const bf16*)x, mean, rstd,
+                                                                    dgamma, dbeta, rows, cols);
+  return check_launch("layernorm_bwd_colred");
 }
 
 extern "C" int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
                               uintptr_t stream) {
   if (cols % 8 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols/ld % 8 != 0");
   if (rows <= 0) return ZPP_OK;
-  const int nblk = (rows + CS_RPB - 1) / CS_RPB;
-  dim3 grid((cols / 8 + 255) / 256, nblk);
-  colsum_partial_kernel<<<grid, 256, 0, STREAM(stream)>>>((const bf16*)dy, ld, workspace, rows, cols);
-  int rc = check_launch("colsum");
-  if (rc) return rc;
-  partial_reduce_kernel<<<(cols + 255) / 256, 256, 0, STREAM(stream)>>>(workspace, nblk, cols, dbias, dbias, cols);
-  return check_launch("colsum_reduce");
+  colred_kernel<false><<<(cols + 31) / 32, 256, 0, STREAM(stream)>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr,
+                                                                     dbias, nullptr, rows, cols);
+  return check_launch("colsum");
 }
 
 extern "C" int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream) {

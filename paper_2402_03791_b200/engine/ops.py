@@ -83,6 +83,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_t: bool = False
     return c
 
 
+def set_cta_group(cg: int) -> None:
+    """GEMM tile policy: 0 auto (CTA pairs when M > 256), 1 single-CTA, 2 prefer pairs."""
+    lib.call("zpp_gemm_set_cta_group", cg)
+
+
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
     _count(1)

@@ -36,10 +36,17 @@ GEMM_SHAPES = [(128, 128, 64), (256, 512, 256), (200, 136, 72), (384, 1024, 320)
                (128, 50304, 256), (1000, 264, 4096)]
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def cta_group(request):
+    ops.set_cta_group(request.param)
+    yield request.param
+    ops.set_cta_group(0)
+
+
 @pytest.mark.parametrize("a_t", [False, True])
 @pytest.mark.parametrize("b_t", [False, True])
 @pytest.mark.parametrize("shape", GEMM_SHAPES, ids=lambda s: "x".join(map(str, s)))
-def test_gemm_layouts(shape, a_t, b_t):
+def test_gemm_layouts(shape, a_t, b_t, cta_group):
     M, N, K = shape
     if (a_t and M % 8) or (b_t and N % 8):
         pytest.skip("MN-major operands need 16-byte row pitch")
@@ -54,7 +61,7 @@ def test_gemm_layouts(shape, a_t, b_t):
     assert rel_err(C, ref) < 1e-5 * math.sqrt(K) + 1e-5
 
 
-def test_gemm_bf16_bias_resid():
+def test_gemm_bf16_bias_resid(cta_group):
     M, N, K = 512, 768, 256
     A, B = bf(M, K), bf(N, K)
     bias, resid = bf(N), bf(M, N)
@@ -64,7 +71,7 @@ def test_gemm_bf16_bias_resid():
     assert rel_err(C, ref) < 1e-2
 
 
-def test_gemm_gelu_and_dgelu():
+def test_gemm_gelu_and_dgelu(cta_group):
     M, N, K = 256, 1024, 512
     A, B, bias = bf(M, K, scale=0.5), bf(N, K, scale=0.1), bf(N)
     G = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
@@ -83,8 +90,8 @@ def test_gemm_gelu_and_dgelu():
     assert rel_err(D, u.grad) < 1e-2
 
 
-def test_gemm_f32_accumulate():
-    M, N, K = 384, 256, 512
+@pytest.mark.parametrize("M,N,K", [(384, 256, 512), (1000, 264, 136)])
+def test_gemm_f32_accumulate(M, N, K, cta_group):
     A, B = bf(K, M), bf(K, N)  # wgrad layout: both MN-major
     C = torch.randn(M, N, device=dev)
     ref = C.clone() + A.float().t() @ B.float()

@@ -1,0 +1,78 @@
+// Microbenchmark: raw tcgen05.mma throughput (smem operands, no TMA / epilogue).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2402_03791_b200/csrc mma_rate.cu -o mma_rate
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+using namespace zpp;
+
+template <int CG, int N, int COMMIT>
+__global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, bar2;
+  __shared__ uint32_t tslot;
+  const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); mbar_init(smem_u32(&bar2), 1 << 20); fence_mbar_init(); }
+  if (warp == 0) { if (CG == 2) tmem_alloc2(smem_u32(&tslot), 256); else tmem_alloc(smem_u32(&tslot), 256); }
+  tc_fence_before();
+  if (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const bool leader = (CG == 1) || cluster_rank() == 0;
+  if (threadIdx.x == 0 && leader) {
+    constexpr uint32_t idesc = make_idesc_bf16(128 * CG, N, false, false);
+    const uint64_t ad = make_sdesc(base, 16, 1024), bd = make_sdesc(base + 16384, 16, 1024);
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (CG == 2) mma_bf16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, 1u);
+        else mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, 1u);
+      }
+      if (COMMIT == 1) { if (CG == 2) mma_commit_2sm(smem_u32(&bar2), 0x3); else mma_commit(smem_u32(&bar2)); }
+      if (COMMIT == 2) { if (CG == 2) mma_commit_2sm(smem_u32(&bar2), 0x1); else mma_commit(smem_u32(&bar2)); }
+    }
+    if (CG == 2) mma_commit_2sm(smem_u32(&bar), 0x3); else mma_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    unsigned long long t1 = clock64();
+    if (blockIdx.x == 0) *cycles = t1 - t0;
+  }
+  if (CG == 2 && !leader && threadIdx.x == 0) mbar_wait(smem_u32(&bar), 0);
+  tc_fence_before();
+  if (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 0) { if (CG == 2) tmem_dealloc2(tmem, 256); else tmem_dealloc(tmem, 256); }
+}
+
+template <int CG, int N, int COMMIT>
+void run(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  auto k = mma_loop<CG, N, COMMIT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = 64 * 1024;
+  cudaLaunchAttribute a[1]; a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = CG; a[0].val.clusterDim.y = 1; a[0].val.clusterDim.z = 1;
+  cfg.attrs = a; cfg.numAttrs = 1;
+  const int iters = 4096;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaLaunchKernelEx(&cfg, k, 16, d);
+  cudaEventRecord(e0);
+  cudaLaunchKernelEx(&cfg, k, iters, d);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaDeviceSynchronize();
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  double macs_per_sm = double(iters) * 4 * 128 * N * 16;  // per SM (each SM owns 128 rows)
+  printf("%-22s %s  %.1f cycles/MMA-instr, %.0f MACs/cycle/SM, %.1f TFLOP/s chip\n", name, cudaGetErrorString(err),
+         double(cyc) / (iters * 4), macs_per_sm / cyc, 2.0 * macs_per_sm * 148 / (ms * 1e-3) / 1e12);
+}
+
+int main() {
+  run<1, 256, 0>("cta1 N256 no-commit");
+  run<2, 256, 0>("cta2 N256 no-commit");
+  run<1, 256, 1>("cta1 N256 commit/kblk");
+  run<2, 256, 1>("cta2 N256 commit mc=3");
+  run<2, 256, 2>("cta2 N256 commit mc=1");
+  return 0;
+}
