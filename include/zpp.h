@@ -58,6 +58,9 @@ int zpp_gemm_set_cta_group(int cg);
 /* ---- causal multi-head attention, qkv packed [b, s, 3, heads, d] bf16 --------- */
 int zpp_attn_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, int head_dim,
                  uintptr_t stream);
+/* attention implementation policy: 0 = auto (tcgen05/TMEM kernels when seq % 128 == 0),
+ * 1 = mma.sync FlashAttention-2 tiles (seq % 64 == 0).  Process-wide. */
+int zpp_attn_set_impl(int impl);
 /* workspace: batch*heads*seq floats (row-wise dO.O) + batch*seq*heads*head_dim floats (dQ accum) */
 int zpp_attn_bwd(const void* qkv, const void* out, const float* lse, const void* dout, void* dqkv,
                  float* workspace, int batch, int seq, int heads, int head_dim, uintptr_t stream);

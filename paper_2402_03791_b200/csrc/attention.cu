@@ -480,14 +480,29 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
   return check_launch("attn_dq_convert");
 }
 
+template <int D>
+int attn_fwd_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s);
+
 }  // namespace zpp
 
 using namespace zpp;
+
+static int g_attn_impl = 0;  // 0 = auto (tcgen05 when seq % 128 == 0), 1 = mma.sync FA2 tiles
+
+extern "C" int zpp_attn_set_impl(int impl) {
+  if (impl < 0 || impl > 1) return set_error(ZPP_ERR_ARG, "attn impl must be 0 or 1");
+  g_attn_impl = impl;
+  return ZPP_OK;
+}
 
 extern "C" int zpp_attn_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, int head_dim,
                             uintptr_t stream) {
   if (seq % 64) return set_error(ZPP_ERR_ARG, "attn: seq must be a multiple of 64");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (g_attn_impl == 0 && seq % 128 == 0) {
+    if (head_dim == 128) return attn_fwd_tc_launch<128>(qkv, out, lse, batch, seq, heads, s);
+    if (head_dim == 64) return attn_fwd_tc_launch<64>(qkv, out, lse, batch, seq, heads, s);
+  }
   if (head_dim == 128) return attn_fwd_launch<128>(qkv, out, lse, batch, seq, heads, s);
   if (head_dim == 64) return attn_fwd_launch<64>(qkv, out, lse, batch, seq, heads, s);
   return set_error(ZPP_ERR_ARG, "attn: head_dim must be 64 or 128");

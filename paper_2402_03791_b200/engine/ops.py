@@ -121,6 +121,11 @@ def gelu(u, g, stream=None):
     lib.call("zpp_gelu_fwd", _p(u), _p(g), u.numel(), _s(stream))
 
 
+def set_attn_impl(impl: int) -> None:
+    """0 auto (tcgen05 kernels when seq % 128 == 0), 1 mma.sync FlashAttention-2 tiles."""
+    lib.call("zpp_attn_set_impl", impl)
+
+
 def attn_fwd(qkv, out, lse, batch, seq, heads, head_dim, stream=None):
     _count(1)
     lib.call("zpp_attn_fwd", _p(qkv), _p(out), _p(lse), batch, seq, heads, head_dim, _s(stream))

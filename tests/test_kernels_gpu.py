@@ -146,9 +146,16 @@ def _attn_ref(qkv, b, s, H, D):
     return o.transpose(1, 2).reshape(b * s, H * D), lse
 
 
+@pytest.fixture(params=[0, 1], ids=["tc", "mma"])
+def attn_impl(request):
+    ops.set_attn_impl(request.param)
+    yield request.param
+    ops.set_attn_impl(0)
+
+
 @pytest.mark.parametrize("D", [64, 128])
-@pytest.mark.parametrize("b,s,H", [(1, 128, 2), (2, 256, 3)])
-def test_attention(b, s, H, D):
+@pytest.mark.parametrize("b,s,H", [(1, 128, 2), (2, 256, 3), (1, 512, 2)])
+def test_attention(b, s, H, D, attn_impl):
     qkv = bf(b * s, 3 * H * D)
     out = torch.empty(b * s, H * D, device=dev, dtype=torch.bfloat16)
     lse = torch.empty(b, H, s, device=dev)
