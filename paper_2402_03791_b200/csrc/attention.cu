@@ -24,6 +24,12 @@ namespace zpp {
 
 typedef __nv_bfloat16 bf16;
 
+template <int D>
+int attn_fwd_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s);
+template <int D>
+int attn_bwd_tc_launch(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
+                       float* dq_acc, int B, int T, int H, cudaStream_t s);
+
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -450,7 +456,7 @@ static int attn_fwd_launch(const void* qkv, void* out, float* lse, int B, int T,
 
 template <int D>
 static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, const void* dout, void* dqkv,
-                           float* ws, int B, int T, int H, cudaStream_t s) {
+                           float* ws, int B, int T, int H, cudaStream_t s, bool use_tc) {
   const int smem = 4 * 64 * D * 2 + 2 * 64 * 64 * 2 + 2 * 64 * 4;
   static bool set = false;
   if (!set) {
@@ -468,10 +474,14 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
                                                                       T, H);
   int rc = check_launch("attn_delta");
   if (rc) return rc;
-  dim3 grid(T / 64, B * H);
-  attn_bwd_kernel<D><<<grid, 128, smem, s>>>((const bf16*)qkv, (const bf16*)dout, lse, delta, (bf16*)dqkv, dq, T, H,
-                                              1.f / sqrtf((float)D));
-  rc = check_launch("attn_bwd");
+  if (use_tc) {
+    rc = attn_bwd_tc_launch<D>(qkv, dout, lse, delta, dqkv, dq, B, T, H, s);
+  } else {
+    dim3 grid(T / 64, B * H);
+    attn_bwd_kernel<D><<<grid, 128, smem, s>>>((const bf16*)qkv, (const bf16*)dout, lse, delta, (bf16*)dqkv, dq, T,
+                                                H, 1.f / sqrtf((float)D));
+    rc = check_launch("attn_bwd");
+  }
   if (rc) return rc;
   const long long n4 = nrows * H * D / 4;
   int blocks = (int)((n4 + 255) / 256);
@@ -480,8 +490,6 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
   return check_launch("attn_dq_convert");
 }
 
-template <int D>
-int attn_fwd_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s);
 
 }  // namespace zpp
 
@@ -516,7 +524,8 @@ extern "C" int zpp_attn_bwd(const void* qkv, const void* out, const float* lse, 
                             float* workspace, int batch, int seq, int heads, int head_dim, uintptr_t stream) {
   if (seq % 64) return set_error(ZPP_ERR_ARG, "attn_bwd: seq must be a multiple of 64");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (head_dim == 128) return attn_bwd_launch<128>(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, s);
-  if (head_dim == 64) return attn_bwd_launch<64>(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, s);
+  const bool tc = g_attn_impl == 0 && seq % 128 == 0;
+  if (head_dim == 128) return attn_bwd_launch<128>(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, s, tc);
+  if (head_dim == 64) return attn_bwd_launch<64>(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, s, tc);
   return set_error(ZPP_ERR_ARG, "attn_bwd: head_dim must be 64 or 128");
 }
