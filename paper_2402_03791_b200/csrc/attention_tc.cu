@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int j = 1; j < 128; ++j) mx = fmaxf(mx, x[j]);
       const float m_new = fmaxf(m_run, mx);
-      const bool rescale = m_new > m_run + 8.f;
+      // tcgen05.ld/st below are warp-collective (.sync.aligned): the rescale decision
+      // must be warp-uniform.  Any lane needing it makes every lane move to its own max.
+      const bool rescale = __any_sync(0xffffffffu, m_new > m_run + 8.f);
       const float m_use = rescale ? m_new : m_run;
       float rs = 0.f;
 #pragma unroll

@@ -85,7 +85,18 @@ def check(rc: int, what: str = "") -> None:
         raise RuntimeError(f"libzpp {what} failed (rc={rc}): {msg}")
 
 
+_DEBUG_SYNC = os.environ.get("ZPP_DEBUG_SYNC") == "1"
+
+
 def call(name: str, *args) -> None:
+    if _DEBUG_SYNC:  # debugging aid: log and synchronize every launch
+        import sys
+        import torch
+        print(f"[zpp] {name}", file=sys.stderr, flush=True)
+        check(getattr(load(), name)(*args), name)
+        torch.cuda.synchronize()
+        print(f"[zpp] {name} done", file=sys.stderr, flush=True)
+        return
     check(getattr(load(), name)(*args), name)
 
 
