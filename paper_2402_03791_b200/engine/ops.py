@@ -18,11 +18,13 @@ class _Profile:
 
     def __init__(self):
         self.active = False
+        self.time_gemms = True
         self.launches = 0
         self._gemms: list = []
 
-    def start(self) -> None:
+    def start(self, time_gemms: bool = True) -> None:
         self.active, self.launches, self._gemms = True, 0, []
+        self.time_gemms = time_gemms
 
     def stop(self):
         """-> (total GEMM FLOPs, summed GEMM launch ms, GEMM launches); synchronizes."""
@@ -68,18 +70,19 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_t: bool = False
     assert (b.shape[0] if b_t else b.shape[1]) == K, "inner dimensions differ"
     assert c.shape[0] == M and c.shape[1] == N
     sid = _s(stream)
-    if PROFILE.active:
+    timed = PROFILE.active and PROFILE.time_gemms
+    if timed:
         ts = torch.cuda.ExternalStream(sid)
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(ts)
     lib.call("zpp_gemm", _p(a), int(a_t), _ld(a), _p(b), int(b_t), _ld(b), _p(c), _ld(c), M, N, K,
              epilogue, _p(bias), _p(resid), _ld(resid) if resid is not None else 0,
              _p(aux), _ld(aux) if aux is not None else 0, sid)
-    if PROFILE.active:
+    if timed:
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(ts)
-        PROFILE.launches += 1
         PROFILE._gemms.append((2.0 * M * N * K, e0, e1))
+    _count(1)
     return c
 
 

@@ -240,3 +240,21 @@ def test_init_param_bit_exact():
     ref = init_values(n, 1234, 777, 0.0, 0.02)
     assert np.array_equal(master.cpu().numpy(), ref)
     assert torch.equal(pb.cpu(), torch.from_numpy(ref).to(torch.bfloat16))
+
+
+@pytest.mark.timeout(120)
+def test_attention_divergent_rescale():
+    """Rows of one warp needing O-rescaling at different key blocks (regression: the
+    rescale branch holds warp-collective tcgen05.ld/st and must stay warp-uniform)."""
+    b, s, H, D = 1, 512, 2, 128
+    qkv = bf(b * s, 3 * H * D).view(b * s, 3, H, D)
+    qkv[:, 0, :, :] *= 0.5
+    qkv[1::2, 0, :, :] *= 4.0          # odd query rows: sharper scores
+    qkv[384:, 1, :, :] *= 3.0          # keys of the last block are larger
+    qkv = qkv.reshape(b * s, 3 * H * D).contiguous()
+    out = torch.empty(b * s, H * D, device=dev, dtype=torch.bfloat16)
+    lse = torch.empty(b, H, s, device=dev)
+    ops.attn_fwd(qkv, out, lse, b, s, H, D)
+    o_ref, lse_ref = _attn_ref(qkv.float(), b, s, H, D)
+    assert rel_err(out, o_ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 2e-2
