@@ -69,13 +69,16 @@ long long zpp_attn_bwd_workspace_floats(int batch, int seq, int heads, int head_
 /* ---- LayerNorm (fp32 statistics) ---------------------------------------------- */
 int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                       int rows, int cols, float eps, uintptr_t stream);
-/* dx = LNbwd(dy) (+ dresid); dgamma/dbeta (fp32) += column sums. workspace: 2*cols*ceil(rows/64) floats */
+/* dx = LNbwd(dy) (+ dresid); dgamma/dbeta (fp32) += column sums (deterministic).
+ * workspace: zpp_layernorm_bwd_workspace_floats() floats, zero-initialised once (it holds
+ * self-re-arming tickets); reusable by later calls on the same stream.  cols % 32 == 0. */
 int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const void* gamma,
                       const void* dresid, void* dx, float* dgamma, float* dbeta, float* workspace, int rows,
                       int cols, uintptr_t stream);
 long long zpp_layernorm_bwd_workspace_floats(int rows, int cols);
 
-/* ---- bias gradient: dbias(f32)[c] += sum_r dy[r,c]; workspace cols*ceil(rows/64) floats */
+/* ---- bias gradient: dbias(f32)[c] += sum_r dy[r,c] (deterministic); workspace as for
+ * zpp_layernorm_bwd (zero-initialised once, zpp_layernorm_bwd_workspace_floats(rows, cols)). */
 int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
                    uintptr_t stream);
 

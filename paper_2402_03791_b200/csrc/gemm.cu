@@ -129,6 +129,19 @@ __device__ __forceinline__ void epi_math(const EpiParams& p, int row, int col, f
   }
 }
 
+// Tile raster: consecutive tiles (processed concurrently by neighbouring SMs) share the
+// operand panel of the LARGER operand, so it streams through L2 once while the smaller
+// operand stays resident.  n_fast: M > N (e.g. wgrad 16384 x 4096) -> walk N first.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, bool n_fast, int& mt, int& nt) {
+  if (n_fast) {
+    mt = tile / num_n;
+    nt = tile % num_n;
+  } else {
+    mt = tile % num_m;
+    nt = tile / num_m;
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -188,14 +201,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_tiles = num_m * num_n;
   const int num_k = (K + GEMM_BK - 1) / GEMM_BK;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
+  const bool n_fast = M > N;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = unit; tile < num_tiles; tile += nunits) {
-        const int m0 = (tile % num_m) * TILE_M + crank * GEMM_BM;
-        const int n0 = (tile / num_m) * BN + crank * BNL;
+        int mt, nt;
+        tile_coords(tile, num_m, num_n, n_fast, mt, nt);
+        const int m0 = mt * TILE_M + crank * GEMM_BM;
+        const int n0 = nt * BN + crank * BNL;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t fb = full_bar(stage);
@@ -271,8 +287,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int row0 = (tile % num_m) * TILE_M + crank * GEMM_BM + q * 32;
-      const int n0 = (tile / num_m) * BN;
+      int mt, nt;
+      tile_coords(tile, num_m, num_n, n_fast, mt, nt);
+      const int row0 = mt * TILE_M + crank * GEMM_BM + q * 32;
+      const int n0 = nt * BN;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;

@@ -158,22 +158,31 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __res
   }
 }
 
-// Column reductions over all rows of a 32-column strip per block (deterministic, one pass):
+// Column reductions (deterministic, one launch):
 //   LN mode : out0[c] += sum_r dy[r,c] * (x[r,c]-mean[r])*rstd[r],  out1[c] += sum_r dy[r,c]
 //   SUM mode: out0[c] += sum_r dy[r,c]                               (bias gradients)
-// 256 threads = 4 column vectors (8 bf16) x 64 row lanes; smem tree over the row lanes.
+// grid = (32-column strips, RS row splits).  256 threads = 4 column vectors (8 bf16) x 64
+// row lanes; each block reduces its rows in fixed order into a workspace slot; the last
+// block of a strip (atomic ticket) adds the RS partials in split order to out.
+constexpr int CR_MAX_SPLIT = 16;
 template <bool LN>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy, long long ld,
                                                      const bf16* __restrict__ x, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, float* __restrict__ out0,
-                                                     float* __restrict__ out1, int rows, int cols) {
-  __shared__ float sh[LN ? 2 : 1][64][33];
+                                                     float* __restrict__ out1, float* __restrict__ ws,
+                                                     unsigned* __restrict__ tickets, int rows, int cols) {
+  constexpr int NO = LN ? 2 : 1;
+  __shared__ float sh[NO][64][33];
+  __shared__ unsigned last;
   const int cv = threadIdx.x & 3, rl = threadIdx.x >> 2;
-  const int c0 = blockIdx.x * 32 + cv * 8;
+  const int strip = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
+  const int c0 = strip * 32 + cv * 8;
+  const int rows_per = (rows + nsplit - 1) / nsplit;
+  const int r_lo = split * rows_per, r_hi = min(rows, r_lo + rows_per);
   float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (c0 < cols) {
 #pragma unroll 4
-    for (int r = rl; r < rows; r += 64) {
+    for (int r = r_lo + rl; r < r_hi; r += 64) {
       float d[8];
       unpack8(*reinterpret_cast<const uint4*>(dy + (long long)r * ld + c0), d);
       if (LN) {
@@ -194,21 +203,38 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     sh[0][rl][cv * 8 + j] = a0[j];
-    if (LN) sh[LN ? 1 : 0][rl][cv * 8 + j] = a1[j];
+    if (LN) sh[NO - 1][rl][cv * 8 + j] = a1[j];
   }
   __syncthreads();
-  // 256 threads: (output k, column c) pairs, each sums 64 row-lane partials in fixed order
-  const int nout = LN ? 2 : 1;
-  for (int idx = threadIdx.x; idx < nout * 32; idx += 256) {
-    const int k = idx / 32, c = idx % 32;
+  // reduce 64 row lanes: thread (k, c) for k < NO, c < 32
+  float part = 0.f;
+  const int k = threadIdx.x / 32, c = threadIdx.x % 32;
+  if (k < NO) {
+    for (int r = 0; r < 64; ++r) part += sh[k][r][c];
+    ws[((long long)split * NO + k) * cols + strip * 32 + c] = part;  // cols % 32 handled by host padding
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[strip], 1u) == (unsigned)(nsplit - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (k < NO) {
     float s = 0.f;
-    for (int r = 0; r < 64; ++r) s += sh[k][r][c];
-    const int col = blockIdx.x * 32 + c;
+    for (int sp = 0; sp < nsplit; ++sp) s += __ldcg(&ws[((long long)sp * NO + k) * cols + strip * 32 + c]);
+    const int col = strip * 32 + c;
     if (col < cols) {
       if (k == 0) out0[col] += s;
       else out1[col] += s;
     }
   }
+  if (threadIdx.x == 0) tickets[strip] = 0;  // re-arm for the next launch (stream-ordered)
+}
+
+static int colred_splits(int rows, int strips) {
+  int s = 1;
+  while (s < CR_MAX_SPLIT && strips * s < 2 * num_sms() && rows / (2 * s) >= 64) s *= 2;
+  return s;
 }
 
 // ----------------------------------------------------------------------------
@@ -410,29 +436,48 @@ extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* b
   return check_launch("layernorm_fwd");
 }
 
-extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) { return 0; }
+// workspace layout for the column reductions: [splits][2][cols_pad] floats + tickets
+extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) {
+  const int cols_pad = (cols + 31) / 32 * 32;
+  return (long long)CR_MAX_SPLIT * 2 * cols_pad + cols_pad / 32;
+}
+
+static int colred_launch(bool ln, const void* dy, long long ld, const void* x, const float* mean, const float* rstd,
+                         float* out0, float* out1, float* ws, int rows, int cols, cudaStream_t st) {
+  const int strips = (cols + 31) / 32;
+  const int cols_pad = strips * 32;
+  const int splits = colred_splits(rows, strips);
+  float* part = ws;
+  unsigned* tickets = reinterpret_cast<unsigned*>(ws + (long long)CR_MAX_SPLIT * 2 * cols_pad);
+  dim3 grid(strips, splits);
+  if (ln)
+    colred_kernel<true><<<grid, 256, 0, st>>>((const bf16*)dy, ld, (const bf16*)x, mean, rstd, out0, out1, part,
+                                              tickets, rows, cols_pad);
+  else
+    colred_kernel<false><<<grid, 256, 0, st>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr, out0, nullptr, part,
+                                               tickets, rows, cols_pad);
+  return check_launch("colred");
+}
 
 extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                                  const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
                                  float* workspace, int rows, int cols, uintptr_t stream) {
-  if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: bad cols");
+  if (cols % 32 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 32 != 0 or > 8192");
+  if (!workspace) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
   layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
                                                              (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc) return rc;
-  colred_kernel<true><<<(cols + 31) / 32, 256, 0, STREAM(stream)>>>((const bf16*)dy, cols, (const bf16*)x, mean, rstd,
-                                                                    dgamma, dbeta, rows, cols);
-  return check_launch("layernorm_bwd_colred");
+  return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, STREAM(stream));
 }
 
 extern "C" int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
                               uintptr_t stream) {
-  if (cols % 8 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols/ld % 8 != 0");
+  if (cols % 32 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols % 32 / ld % 8 != 0");
+  if (!workspace) return set_error(ZPP_ERR_ARG, "colsum: workspace required");
   if (rows <= 0) return ZPP_OK;
-  colred_kernel<false><<<(cols + 31) / 32, 256, 0, STREAM(stream)>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr,
-                                                                     dbias, nullptr, rows, cols);
-  return check_launch("colsum");
+  return colred_launch(false, dy, ld, nullptr, nullptr, nullptr, dbias, nullptr, workspace, rows, cols, STREAM(stream));
 }
 
 extern "C" int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream) {

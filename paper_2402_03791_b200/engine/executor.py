@@ -115,8 +115,9 @@ class Runtime:
         self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
         self.s_act_send, self.s_act_recv, self.s_grad_send, self.s_grad_recv = mk(), mk(), mk(), mk()
         T, h = spec.tokens_per_microbatch, spec.hidden
-        self.ln_ws = torch.empty(ops.layernorm_bwd_workspace(T, h), dtype=F32, device=self.dev)
-        self.cs_ws = torch.empty(ops.colsum_workspace(T, 4 * h), dtype=F32, device=self.dev)
+        # column-reduction workspaces carry re-armed tickets: zero them once
+        self.ln_ws = torch.zeros(ops.layernorm_bwd_workspace(T, h), dtype=F32, device=self.dev)
+        self.cs_ws = torch.zeros(ops.colsum_workspace(T, 4 * h), dtype=F32, device=self.dev)
         self.attn_ws = torch.empty(ops.attn_bwd_workspace(spec.microbatch_samples, spec.seq_len,
                                                           spec.heads, spec.head_dim),
                                    dtype=F32, device=self.dev)

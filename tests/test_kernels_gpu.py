@@ -119,20 +119,23 @@ def test_layernorm(cols):
     dx = torch.empty_like(x)
     dg = torch.zeros(cols, device=dev)
     db = torch.zeros(cols, device=dev)
-    ws = torch.empty(ops.layernorm_bwd_workspace(rows, cols), device=dev)
+    ws = torch.zeros(ops.layernorm_bwd_workspace(rows, cols), device=dev)
     ops.layernorm_bwd(dy, x, mean, rstd, g, dx, dg, db, ws, dresid=dres)
     assert rel_err(dx, xf.grad + dres.float()) < 1e-2
     assert rel_err(dg, gf.grad) < 1e-4
     assert rel_err(db, bff.grad) < 1e-4
 
 
-def test_colsum():
-    dy = bf(1000, 768)
-    acc = torch.randn(768, device=dev)
+@pytest.mark.parametrize("rows,cols", [(1000, 768), (2048, 16384), (64, 96)])
+def test_colsum(rows, cols):
+    dy = bf(rows, cols)
+    acc = torch.randn(cols, device=dev)
     ref = acc + dy.float().sum(0)
-    ws = torch.empty(ops.colsum_workspace(1000, 768), device=dev)
+    ws = torch.zeros(ops.colsum_workspace(rows, cols), device=dev)
     ops.colsum_acc(dy, acc, ws)
     assert rel_err(acc, ref) < 1e-5
+    ops.colsum_acc(dy, acc, ws)  # tickets re-armed: a second launch accumulates again
+    assert rel_err(acc, ref + dy.float().sum(0)) < 1e-5
 
 
 def _attn_ref(qkv, b, s, H, D):

@@ -5,7 +5,7 @@
 #include "ptx.cuh"
 using namespace zpp;
 
-template <int CG, int N, int COMMIT>
+template <int CG, int N, int COMMIT, bool AMN = false, bool BMN = false>
 __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, bar2;
@@ -20,14 +20,15 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
   const uint32_t tmem = tslot;
   const bool leader = (CG == 1) || cluster_rank() == 0;
   if (threadIdx.x == 0 && leader) {
-    constexpr uint32_t idesc = make_idesc_bf16(128 * CG, N, false, false);
-    const uint64_t ad = make_sdesc(base, 16, 1024), bd = make_sdesc(base + 16384, 16, 1024);
+    constexpr uint32_t idesc = make_idesc_bf16(128 * CG, N, AMN, BMN);
+    const uint64_t ad = make_sdesc(base, AMN ? 8192 : 16, 1024), bd = make_sdesc(base + 16384, BMN ? 8192 : 16, 1024);
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (CG == 2) mma_bf16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, 1u);
-        else mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, 1u);
+        const uint64_t ka = AMN ? (uint64_t)(128 * k) : (uint64_t)(2 * k), kb = BMN ? (uint64_t)(128 * k) : (uint64_t)(2 * k);
+        if (CG == 2) mma_bf16_2sm(tmem, ad + ka, bd + kb, idesc, 1u);
+        else mma_bf16(tmem, ad + ka, bd + kb, idesc, 1u);
       }
       if (COMMIT == 1) { if (CG == 2) mma_commit_2sm(smem_u32(&bar2), 0x3); else mma_commit(smem_u32(&bar2)); }
       if (COMMIT == 2) { if (CG == 2) mma_commit_2sm(smem_u32(&bar2), 0x1); else mma_commit(smem_u32(&bar2)); }
@@ -43,11 +44,11 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
   if (warp == 0) { if (CG == 2) tmem_dealloc2(tmem, 256); else tmem_dealloc(tmem, 256); }
 }
 
-template <int CG, int N, int COMMIT>
+template <int CG, int N, int COMMIT, bool AMN = false, bool BMN = false>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 8);
-  auto k = mma_loop<CG, N, COMMIT>;
+  auto k = mma_loop<CG, N, COMMIT, AMN, BMN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = 64 * 1024;
@@ -69,10 +70,9 @@ void run(const char* name) {
 }
 
 int main() {
-  run<1, 256, 0>("cta1 N256 no-commit");
-  run<2, 256, 0>("cta2 N256 no-commit");
-  run<1, 256, 1>("cta1 N256 commit/kblk");
-  run<2, 256, 1>("cta2 N256 commit mc=3");
-  run<2, 256, 2>("cta2 N256 commit mc=1");
+  run<2, 256, 1, false, false>("cta2 K/K");
+  run<2, 256, 1, false, true>("cta2 K/MN");
+  run<2, 256, 1, true, true>("cta2 MN/MN");
+  run<1, 256, 1, true, true>("cta1 MN/MN");
   return 0;
 }
