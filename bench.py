@@ -24,6 +24,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # see zpp_preload_kernels
 import statistics
 import subprocess
 import sys

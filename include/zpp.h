@@ -40,6 +40,11 @@ const char* zpp_last_error(void);
 int zpp_num_sms(void);
 int zpp_version(void);
 
+/* Load every kernel now.  Call once per process before any NCCL traffic: with CUDA lazy
+ * loading a kernel's first launch synchronises the context, which deadlocks against NCCL
+ * kernels that spin on a peer rank. */
+int zpp_preload_kernels(void);
+
 /* cudaMemsetAsync(ptr, 0, bytes) on stream (grad buffers, loss accumulator) */
 int zpp_zero(void* ptr, long long bytes, uintptr_t stream);
 

@@ -495,6 +495,33 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
 
 using namespace zpp;
 
+namespace zpp {
+int attention_tc_preload();
+int gemm_preload();
+int kernels_preload();
+}  // namespace zpp
+
+// Force-load every kernel of the library (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which needs a context-wide synchronisation: that
+// deadlocks against NCCL kernels spinning on a peer rank).
+extern "C" int zpp_preload_kernels(void) {
+  int rc = gemm_preload();
+  if (rc) return rc;
+  rc = attention_tc_preload();
+  if (rc) return rc;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, attn_fwd_kernel<64>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, attn_fwd_kernel<128>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, attn_bwd_kernel<64>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, attn_bwd_kernel<128>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, attn_delta_kernel<64>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, attn_delta_kernel<128>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, dq_convert_kernel<64>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, dq_convert_kernel<128>);
+  if (e != cudaSuccess) return set_cuda_error(e, "attention preload");
+  return kernels_preload();
+}
+
 static int g_attn_impl = 0;  // 0 = auto (tcgen05 when seq % 128 == 0), 1 = mma.sync FA2 tiles
 
 extern "C" int zpp_attn_set_impl(int impl) {

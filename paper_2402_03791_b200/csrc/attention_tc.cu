@@ -547,4 +547,13 @@ template int attn_bwd_tc_launch<64>(const void*, const void*, const float*, cons
 template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, const float*, void*, float*, int, int,
                                      int, cudaStream_t);
 
+int attention_tc_preload() {
+  cudaError_t e = cudaSuccess;
+  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_fwd_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcFwdCfg<64>::SMEM));
+  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_fwd_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcFwdCfg<128>::SMEM));
+  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_bwd_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcBwdCfg<64>::SMEM));
+  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_bwd_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcBwdCfg<128>::SMEM));
+  return e == cudaSuccess ? ZPP_OK : set_cuda_error(e, "attention_tc preload");
+}
+
 }  // namespace zpp

@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "ptx.cuh"
 #include "zpp_internal.h"
@@ -405,7 +406,12 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
     attr_set = true;
   }
   const int tiles = ((M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((N + BN - 1) / BN);
-  const int units = num_sms() / CG;
+  static int reserve = -1;
+  if (reserve < 0) {
+    const char* e = getenv("ZPP_GEMM_RESERVE_SMS");
+    reserve = e ? atoi(e) : 0;
+  }
+  const int units = (num_sms() - reserve) / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -422,6 +428,26 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return check_launch("gemm_tcgen05");
+}
+
+template <int BN, bool A_MN, bool B_MN, int CG>
+static int preload_one() {
+  cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, A_MN, B_MN, CG>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, CG>::SMEM);
+  return e == cudaSuccess ? ZPP_OK : set_cuda_error(e, "gemm preload");
+}
+
+int gemm_preload() {
+  int rc = 0;
+  rc |= preload_one<256, false, false, 1>(); rc |= preload_one<256, false, true, 1>();
+  rc |= preload_one<256, true, false, 1>();  rc |= preload_one<256, true, true, 1>();
+  rc |= preload_one<128, false, false, 1>(); rc |= preload_one<128, false, true, 1>();
+  rc |= preload_one<128, true, false, 1>();  rc |= preload_one<128, true, true, 1>();
+  rc |= preload_one<256, false, false, 2>(); rc |= preload_one<256, false, true, 2>();
+  rc |= preload_one<256, true, false, 2>();  rc |= preload_one<256, true, true, 2>();
+  rc |= preload_one<128, false, false, 2>(); rc |= preload_one<128, false, true, 2>();
+  rc |= preload_one<128, true, false, 2>();  rc |= preload_one<128, true, true, 2>();
+  return rc;
 }
 
 template <bool A_MN, bool B_MN>

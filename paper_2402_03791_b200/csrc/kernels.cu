@@ -421,6 +421,20 @@ static int grid_for(long long n, int per_block) {
   return static_cast<int>(g);
 }
 
+int kernels_preload() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {(const void*)layernorm_fwd_kernel, (const void*)layernorm_bwd_dx_kernel,
+                       (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
+                       (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_kernel,
+                       (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel,
+                       (const void*)adamw_kernel, (const void*)init_param_kernel};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return set_cuda_error(e, "kernels preload");
+  }
+  return ZPP_OK;
+}
+
 }  // namespace zpp
 
 using namespace zpp;

@@ -23,6 +23,7 @@ schedule validates (`validation.py:99-135`) before touching the GPU.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -35,6 +36,7 @@ from . import lib, ops
 from .model import GPTSpec, StageLayout, init_offset, shard_init_ranges, stage_layout
 
 BF16, F32 = torch.bfloat16, torch.float32
+_TRACE = os.environ.get("ZPP_TRACE") == "1"
 
 
 @dataclass
@@ -105,6 +107,7 @@ class Runtime:
         self.dev = torch.device("cuda", device)
         torch.cuda.set_device(self.dev)
         lib.load()
+        lib.call("zpp_preload_kernels")  # no lazy kernel loading once NCCL kernels can spin
         self.tasks = list(sched.per_device[self.p])
         self.local_stages = placement.device_stages(self.p)
         self.stages: dict[int, _Stage] = {}
@@ -224,9 +227,14 @@ class Runtime:
         comp = self.s_comp
         comp.wait_stream(torch.cuda.current_stream(self.dev))
         t_start = self._record(comp, True)
+        trace = _TRACE and self.step_count <= 2
         with torch.cuda.stream(comp):
             ops.zero(self.loss_sum, stream=comp)
             for task in self.tasks:
+                if trace:
+                    print(f"[r{self.rank} {time.perf_counter():.3f}] {task.task_id} "
+                          f"alloc={torch.cuda.memory_allocated(self.dev) / 1e9:.1f}G "
+                          f"reserved={torch.cuda.memory_reserved(self.dev) / 1e9:.1f}G", flush=True)
                 stream = self._stream_of(task)
                 e0 = self._record(stream, True) if self.timeline else None
                 self._run(task)

@@ -43,6 +43,7 @@ _SIGS = {
                           c_stream]),
     "zpp_init_param": (c_int, [P, P, c_size, c_ulonglong, c_size, c_float, c_float, c_stream]),
     "zpp_zero": (c_int, [P, c_size, c_stream]),
+    "zpp_preload_kernels": (c_int, []),
     "zpp_nccl_load": (c_int, [c_char_p]),
     "zpp_nccl_unique_id": (c_int, [c_char_p]),
     "zpp_comm_init": (c_int, [c_char_p, c_int, c_int, POINTER(c_void_p)]),

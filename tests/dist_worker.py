@@ -4,6 +4,8 @@ usage: torchrun --nproc-per-node P*D dist_worker.py P D B U V OUTDIR
 """
 
 import os
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # see zpp_preload_kernels
 import sys
 
 import torch

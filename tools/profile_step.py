@@ -51,3 +51,21 @@ print(f"{'kernel':40s} {'calls':>6s} {'ms':>9s} {'share':>6s}")
 for k, v in tot.most_common():
     print(f"{k[:40]:40s} {cnt[k]:6d} {v/1e3:9.2f} {100*v/all_us:5.1f}%")
 print(f"total kernel time {all_us/1e3:.1f} ms")
+
+# inter-kernel idle gaps on the compute stream (CUPTI timestamps)
+evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
+             key=lambda e: e.time_range.start)
+gaps = []
+for a, b in zip(evs, evs[1:]):
+    g = b.time_range.start - a.time_range.end
+    if g > 0:
+        gaps.append((g, a.name.split("(")[0][:30], b.name.split("(")[0][:30]))
+span = evs[-1].time_range.end - evs[0].time_range.start
+tot_gap = sum(g for g, _, _ in gaps)
+print(f"span {span/1e3:.1f} ms, kernel-to-kernel idle {tot_gap/1e3:.1f} ms over {len(gaps)} gaps "
+      f"(median {sorted(g for g,_,_ in gaps)[len(gaps)//2]:.2f} us)")
+by = collections.Counter()
+for g, a, b in gaps:
+    by[(a, b)] += g
+for (a, b), g in by.most_common(8):
+    print(f"  {g/1e3:7.2f} ms  {a} -> {b}")
