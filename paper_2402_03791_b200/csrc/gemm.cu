@@ -57,7 +57,7 @@ struct GemmCfg {
   static constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;  // 4 epilogue warps x 2 buffers
   static constexpr int STAGES = (224 * 1024 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers, tile ring*/;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -146,7 +146,8 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, bool
 template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmC, int M, int N, int K, EpiParams ep) {
+                        const __grid_constant__ CUtensorMap tmC, int M, int N, int K, EpiParams ep,
+                        unsigned* __restrict__ sched) {
   using Cfg = GemmCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int TILE_M = GEMM_BM * CG;
@@ -164,6 +165,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * STAGES + 2 + a); };
+  // dynamic tile scheduler: ring of RING tile indices fed by the leader's producer
+  constexpr int RING = 4;
+  const uint32_t ring_base = bars + 256;  // RING x u32 tile ids, then full/empty barriers
+  auto ring_slot = [&](int s) { return ring_base + 4u * s; };
+  auto ring_full = [&](int s) { return ring_base + 32 + 8u * s; };
+  auto ring_empty = [&](int s) { return ring_base + 32 + 8u * (RING + s); };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -185,6 +192,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 128 * CG);  // every epilogue thread of the pair
     }
+    for (int r = 0; r < RING; ++r) {
+      mbar_init(ring_full(r), 1);
+      // readers: leader MMA + 4 epilogue warps (+ peer producer + 4 peer epilogue warps)
+      mbar_init(ring_empty(r), CG == 2 ? 10 : 5);
+    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -201,14 +213,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_k = (K + GEMM_BK - 1) / GEMM_BK;
-  const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
   const bool n_fast = M > N;
+  // Readers take the next tile id from the ring (leader's ring_empty counts the readers).
+  const uint32_t ring_empty_leader = (CG == 2) ? map_cta(ring_empty(0), 0) : ring_empty(0);
+  auto next_tile = [&](int it, bool arrive) -> int {
+    const int slot = it % RING;
+    if (CG == 2) mbar_wait_cluster(ring_full(slot), (it / RING) & 1);
+    else mbar_wait(ring_full(slot), (it / RING) & 1);
+    const int t = static_cast<int>(ld_shared_u32(ring_slot(slot)));
+    if (arrive) {
+      if (CG == 2) mbar_arrive_remote(ring_empty_leader + 8u * slot);
+      else mbar_arrive(ring_empty(slot));
+    }
+    return t;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits) {
+      for (int it = 0;; ++it) {
+        int tile;
+        if (leader) {  // the scheduler: grab a tile and publish it to every role of the pair
+          const int slot = it % RING;
+          mbar_wait(ring_empty(slot), ((it / RING) & 1) ^ 1);
+          tile = static_cast<int>(atomicAdd(sched, 1u));
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ring_slot(slot)), "r"(tile) : "memory");
+          mbar_arrive(ring_full(slot));
+          if (CG == 2) {
+            st_cluster_u32(map_cta(ring_slot(slot), 1), static_cast<uint32_t>(tile));
+            mbar_arrive_cluster(map_cta(ring_full(slot), 1));
+          }
+        } else {
+          tile = next_tile(it, true);
+        }
+        if (tile >= num_tiles) break;
         int mt, nt;
         tile_coords(tile, num_m, num_n, n_fast, mt, nt);
         const int m0 = mt * TILE_M + crank * GEMM_BM;
@@ -250,8 +289,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       constexpr uint32_t B_KSTEP = B_MN ? 16 * 128 : 32;
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
+      for (int it = 0;; ++it) {
+        const int tile = next_tile(it, true);
+        if (tile >= num_tiles) break;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(tempty_bar(acc), acc_phase ^ 1);
@@ -284,8 +324,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool f32out = (mode == ZPP_EPI_F32 || mode == ZPP_EPI_F32_ACC);
     const uint32_t ebuf0 = sE + q * 2 * EPI_BUF;
     const uint32_t tempty_leader = (CG == 2) ? map_cta(tempty_bar(0), 0) : tempty_bar(0);
-    int it = 0, nb = 0;  // nb: staging buffers used so far (ring of 2)
-    for (int tile = unit; tile < num_tiles; tile += nunits, ++it) {
+    int nb = 0;  // nb: staging buffers used so far (ring of 2)
+    for (int it = 0;; ++it) {
+      const int tile = next_tile(it, false);
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_remote(ring_empty_leader + 8u * (it % RING));
+        else mbar_arrive(ring_empty(it % RING));
+      }
+      if (tile >= num_tiles) break;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       int mt, nt;
@@ -363,6 +410,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (CG == 2) tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
     else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
+  if (threadIdx.x == 0) {  // the last CTA out re-arms the scheduler slot (stream-ordered reuse)
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -376,6 +431,21 @@ static int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const v
   cuuint32_t estr[2] = {1, 1};
   return encode_tensor_map(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                            CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Scheduler counters: [tile counter, CTAs done] per launch slot, zeroed once and re-armed
+// by the last CTA of each launch; slots rotate so concurrent launches on other streams
+// do not share one.
+static unsigned* sched_slot() {
+  constexpr int NSLOT = 256;
+  static unsigned* buf = nullptr;
+  static unsigned next = 0;
+  if (!buf) {
+    if (cudaMalloc(&buf, NSLOT * 2 * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    cudaMemset(buf, 0, NSLOT * 2 * sizeof(unsigned));
+    cudaDeviceSynchronize();
+  }
+  return buf + 2 * (next++ % NSLOT);
 }
 
 template <int BN, bool A_MN, bool B_MN, int CG>
@@ -425,7 +495,9 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep);
+  unsigned* sched = sched_slot();
+  if (!sched) return set_error(ZPP_ERR_CUDA, "gemm: scheduler buffer allocation failed");
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep, sched);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return check_launch("gemm_tcgen05");
 }
