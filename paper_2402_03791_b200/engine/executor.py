@@ -89,8 +89,6 @@ class Runtime:
             raise ValueError("ModelSpec and GPTSpec disagree on L / h / s")
         if cfg.microbatch_samples != spec.microbatch_samples:
             raise ValueError("ParallelConfig.microbatch_samples != GPTSpec.microbatch_samples")
-        if cfg.recompute is RecomputeMode.FULL and cfg.stages_per_device > 1:
-            raise NotImplementedError("recompute=full (R tasks) is a 'next' row (SURVEY.md 8f)")
         if cfg.inter_node_dp > 1:
             raise NotImplementedError("inter_node_dp > 1 (outer DP / ZeRO-1) is a 'next' row")
         bad = validate(sched, placement, cfg)
@@ -273,6 +271,8 @@ class Runtime:
             self._backward_input(task.stage, task.microbatch)
         elif k is TaskKind.W:
             self._backward_weight(task.stage, task.microbatch)
+        elif k is TaskKind.R:
+            self._recompute(task.stage, task.microbatch)
         elif k is TaskKind.AG_PARAM:
             self._all_gather(task.stage)
         elif k is TaskKind.RS_GRAD:
@@ -358,21 +358,18 @@ class Runtime:
         return buf
 
     # ------------------------------------------------------------------ stage math
-    def _forward(self, s: int, m: int) -> None:
+    def _recomputed(self, s: int) -> bool:
+        """Stages whose activations are recomputed by an R task (schedules.py:454-474)."""
+        P, V = self.P, self.cfg.stages_per_device
+        return self.cfg.recompute is RecomputeMode.FULL and V > 1 and s // P < V - 1
+
+    def _stage_layers(self, st: "_Stage", x: torch.Tensor):
+        """Run the stage's transformer blocks on x; returns (per-layer stash, output)."""
         spec = self.spec
-        st = self.stages[s]
-        self._use_params(st)
         T, h, H, dh = spec.tokens_per_microbatch, spec.hidden, spec.heads, spec.head_dim
         b, sl = spec.microbatch_samples, spec.seq_len
         P = st.p
         e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
-        if s == 0:
-            x = e(T, h)
-            ops.embed_fwd(self._ids[m], P[("wte", None)], P[("wpe", None)], x, sl)
-        elif self._dev_of(s - 1) == self.p:
-            x = self._local_act.pop((s, m))
-        else:
-            x = self._recv("act", (T, h), self._dev_of(s - 1))
         layers = []
         lo, hi = st.lay.layers
         for l in range(lo, hi):
@@ -393,19 +390,48 @@ class Runtime:
             layers.append({"x": x, "xn1": xn1, "mu1": mu1, "r1": r1, "qkv": qkv, "o": o, "lse": lse,
                            "x1": x1, "xn2": xn2, "mu2": mu2, "r2": r2, "u": u, "g": g})
             x = x2
-        stash = {"layers": layers}
+        return layers, x
+
+    def _forward(self, s: int, m: int) -> None:
+        spec = self.spec
+        st = self.stages[s]
+        self._use_params(st)
+        T, h = spec.tokens_per_microbatch, spec.hidden
+        P = st.p
+        e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
+        if s == 0:
+            x = e(T, h)
+            ops.embed_fwd(self._ids[m], P[("wte", None)], P[("wpe", None)], x, spec.seq_len)
+        elif self._dev_of(s - 1) == self.p:
+            x = self._local_act.pop((s, m))
+        else:
+            x = self._recv("act", (T, h), self._dev_of(s - 1))
+        layers, out = self._stage_layers(st, x)
+        if self._recomputed(s):
+            stash = {"x_in": x}  # boundary slab only; R(s, m) rebuilds the rest
+            del layers
+        else:
+            stash = {"layers": layers}
         if s == self.S - 1:
             xf, muf, rf = e(T, h), e(T, dt=F32), e(T, dt=F32)
-            ops.layernorm_fwd(x, P[("lnf_g", None)], P[("lnf_b", None)], xf, muf, rf, spec.ln_eps)
+            ops.layernorm_fwd(out, P[("lnf_g", None)], P[("lnf_b", None)], xf, muf, rf, spec.ln_eps)
             logits = e(T, spec.vocab)
             ops.gemm(xf, P[("w_lm", None)], logits)
             ops.xent(logits, self._labels[m], self.loss_sum, self._grad_scale)
-            stash.update(xlast=x, xf=xf, muf=muf, rf=rf, dlogits=logits)
+            stash.update(xlast=out, xf=xf, muf=muf, rf=rf, dlogits=logits)
         elif self._dev_of(s + 1) == self.p:
-            self._local_act[(s + 1, m)] = x
+            self._local_act[(s + 1, m)] = out
         else:
-            self._send("act", x, self._dev_of(s + 1))
+            self._send("act", out, self._dev_of(s + 1))
         self._stash[(s, m)] = stash
+
+    def _recompute(self, s: int, m: int) -> None:
+        """R task: re-run the stage forward from the stashed input (schedules.py:466-472)."""
+        st = self.stages[s]
+        self._use_params(st)
+        stash = self._stash[(s, m)]
+        layers, _ = self._stage_layers(st, stash.pop("x_in"))
+        stash["layers"] = layers
 
     def _backward_input(self, s: int, m: int) -> None:
         spec = self.spec

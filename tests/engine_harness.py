@@ -24,10 +24,10 @@ GRAD_COS = 0.999
 GRAD_MAXABS = 2e-2
 
 
-def build(spec: GPTSpec, P: int, D: int, B: int, U: int, V: int):
+def build(spec: GPTSpec, P: int, D: int, B: int, U: int, V: int, **cfg_kw):
     model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
     cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V,
-                         microbatch_samples=spec.microbatch_samples)
+                         microbatch_samples=spec.microbatch_samples, **cfg_kw)
     pl = make_placement(cfg, model)
     return model, cfg, pl, generate(model, cfg, pl)
 
@@ -57,8 +57,8 @@ def rank_tokens(tokens_step: torch.Tensor, z: int):
     return t[:, :, :-1].reshape(B, -1).contiguous(), t[:, :, 1:].reshape(B, -1).contiguous()
 
 
-def run_engine_step(spec, P, D, B, U, V, rank=0, world=1, steps=1, timeline=True):
-    model, cfg, pl, sched = build(spec, P, D, B, U, V)
+def run_engine_step(spec, P, D, B, U, V, rank=0, world=1, steps=1, timeline=True, **cfg_kw):
+    model, cfg, pl, sched = build(spec, P, D, B, U, V, **cfg_kw)
     rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=timeline)
     tokens = make_tokens(steps, D, B, spec.microbatch_samples, spec.seq_len, spec.vocab)
     out = []

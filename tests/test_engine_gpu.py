@@ -30,6 +30,20 @@ def test_single_gpu_step_matches_oracle(B, U, V):
     assert starts == sorted(starts)
 
 
+@pytest.mark.parametrize("B,U,V", [(8, 4, 2), (4, 4, 4)])
+def test_recompute_step_matches_oracle(B, U, V):
+    """R tasks (recompute=full) re-run early-round stage forwards before B (schedules.py:454-474)."""
+    from paper_2402_03791_b200 import RecomputeMode, TaskKind
+    spec = GPTSpec.tiny()
+    rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, 1, 1, B, U, V,
+                                                                recompute=RecomputeMode.FULL)
+    assert any(t.kind is TaskKind.R for t in sched.per_device[0])
+    loss = res[0].loss_sum.item() / (B * spec.tokens_per_microbatch)
+    loss_o, grads_o, new_o = oracle_for(spec, cfg, pl, tokens[0])
+    assert abs(loss - loss_o) / loss_o <= LOSS_RTOL, (loss, loss_o)
+    assert not compare_shards(spec, cfg, pl, rt, grads_o, new_o)
+
+
 def test_loss_decreases_over_steps():
     spec = GPTSpec.tiny(lr=1e-3)
     B = 4
