@@ -95,6 +95,144 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
   }
 }
 
+// Warp-per-row LayerNorm (h = 256 * HV): the row stays packed in registers (HV uint4 per
+// lane), every load/store instruction of a warp covers 512 contiguous bytes, and the
+// reductions are warp shuffles only (no block barriers), so many rows are in flight per SM.
+template <int HV>
+__global__ void __launch_bounds__(256, HV <= 12 ? 2 : 1) ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                          const bf16* __restrict__ b, bf16* __restrict__ y,
+                                                          float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                          int rows, float eps) {
+  constexpr int COLS = HV * 256;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (long long)row * COLS);
+    uint4 raw[HV];
+#pragma unroll
+    for (int i = 0; i < HV; ++i) raw[i] = __ldcs(xr + i * 32 + lane);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < HV; ++i) {
+      float f[8];
+      unpack8(raw[i], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += f[j];
+    }
+    const float mu = warp_sum(s) * (1.f / COLS);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < HV; ++i) {
+      float f[8];
+      unpack8(raw[i], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { const float d = f[j] - mu; q += d * d; }
+    }
+    const float rs = rsqrtf(warp_sum(q) * (1.f / COLS) + eps);
+    uint4* yr = reinterpret_cast<uint4*>(y + (long long)row * COLS);
+#pragma unroll 2
+    for (int i = 0; i < HV; ++i) {
+      float f[8], gg[8], bb[8], o[8];
+      unpack8(raw[i], f);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i * 32 + lane), gg);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(b) + i * 32 + lane), bb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (f[j] - mu) * rs * gg[j] + bb[j];
+      yr[i * 32 + lane] = pack8(o);
+    }
+    if (lane == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+  }
+}
+
+template <int HV>
+__global__ void __launch_bounds__(256) ln_bwd_dx_warp_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                             const float* __restrict__ mean,
+                                                             const float* __restrict__ rstd,
+                                                             const bf16* __restrict__ g,
+                                                             const bf16* __restrict__ dres, bf16* __restrict__ dx,
+                                                             int rows) {
+  constexpr int COLS = HV * 256;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (long long)row * COLS);
+    const uint4* dr = reinterpret_cast<const uint4*>(dy + (long long)row * COLS);
+    uint4 rx[HV], rd[HV];
+#pragma unroll
+    for (int i = 0; i < HV; ++i) {
+      rx[i] = __ldg(xr + i * 32 + lane);
+      rd[i] = __ldg(dr + i * 32 + lane);
+    }
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 2
+    for (int i = 0; i < HV; ++i) {
+      float xv[8], dv[8], gg[8];
+      unpack8(rx[i], xv);
+      unpack8(rd[i], dv);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i * 32 + lane), gg);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float dg = dv[j] * gg[j];
+        s1 += dg;
+        s2 += dg * (xv[j] - mu) * rs;
+      }
+    }
+    const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
+    uint4* o = reinterpret_cast<uint4*>(dx + (long long)row * COLS);
+    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (long long)row * COLS) : nullptr;
+#pragma unroll 2
+    for (int i = 0; i < HV; ++i) {
+      float xv[8], dv[8], gg[8], out[8];
+      unpack8(rx[i], xv);
+      unpack8(rd[i], dv);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i * 32 + lane), gg);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out[j] = rs * (dv[j] * gg[j] - m1 - (xv[j] - mu) * rs * m2);
+      if (rr) {
+        float rv[8];
+        unpack8(__ldcs(rr + i * 32 + lane), rv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out[j] += rv[j];
+      }
+      o[i * 32 + lane] = pack8(out);
+    }
+  }
+}
+
+#define ZPP_LN_HV_LIST(X) X(1) X(2) X(4) X(8) X(12) X(16) X(20) X(24)
+
+static bool ln_warp_fwd(int hv, const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mu, float* rs, int rows,
+                        float eps, cudaStream_t st) {
+  const int grid = (rows + 7) / 8;
+  switch (hv) {
+#define ZPP_CASE(H) \
+  case H:           \
+    ln_fwd_warp_kernel<H><<<grid, 256, 0, st>>>(x, g, b, y, mu, rs, rows, eps); \
+    return true;
+    ZPP_LN_HV_LIST(ZPP_CASE)
+#undef ZPP_CASE
+    default:
+      return false;
+  }
+}
+
+static bool ln_warp_bwd(int hv, const bf16* dy, const bf16* x, const float* mu, const float* rs, const bf16* g,
+                        const bf16* dres, bf16* dx, int rows, cudaStream_t st) {
+  const int grid = (rows + 7) / 8;
+  switch (hv) {
+#define ZPP_CASE(H) \
+  case H:           \
+    ln_bwd_dx_warp_kernel<H><<<grid, 256, 0, st>>>(dy, x, mu, rs, g, dres, dx, rows); \
+    return true;
+    ZPP_LN_HV_LIST(ZPP_CASE)
+#undef ZPP_CASE
+    default:
+      return false;
+  }
+}
+
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
 // the two row sums fused into a single float2 block reduction.
 __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
@@ -161,34 +299,37 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __res
 // Column reductions (deterministic, one launch):
 //   LN mode : out0[c] += sum_r dy[r,c] * (x[r,c]-mean[r])*rstd[r],  out1[c] += sum_r dy[r,c]
 //   SUM mode: out0[c] += sum_r dy[r,c]                               (bias gradients)
-// grid = (32-column strips, RS row splits).  256 threads = 4 column vectors (8 bf16) x 64
-// row lanes; each block reduces its rows in fixed order into a workspace slot; the last
-// block of a strip (atomic ticket) adds the RS partials in split order to out.
-constexpr int CR_MAX_SPLIT = 16;
+// grid = (256-column strips, row splits).  256 threads = 32 column vectors (8 bf16) x 8 row
+// lanes, so every warp reads 512 contiguous bytes of one row.  Each block reduces its rows in
+// fixed order into a workspace slot; the last block of a strip (atomic ticket) adds the
+// split partials in split order to out.
+constexpr int CR_MAX_SPLIT = 32;
+constexpr int CR_COLS = 256;
 template <bool LN>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy, long long ld,
                                                      const bf16* __restrict__ x, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, float* __restrict__ out0,
                                                      float* __restrict__ out1, float* __restrict__ ws,
-                                                     unsigned* __restrict__ tickets, int rows, int cols) {
+                                                     unsigned* __restrict__ tickets, int rows, int cols,
+                                                     int ws_ld) {
   constexpr int NO = LN ? 2 : 1;
-  __shared__ float sh[NO][64][33];
+  __shared__ float sh[NO][8][CR_COLS + 4];
   __shared__ unsigned last;
-  const int cv = threadIdx.x & 3, rl = threadIdx.x >> 2;
+  const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int strip = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
-  const int c0 = strip * 32 + cv * 8;
+  const int c0 = strip * CR_COLS + cv * 8;
   const int rows_per = (rows + nsplit - 1) / nsplit;
   const int r_lo = split * rows_per, r_hi = min(rows, r_lo + rows_per);
   float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (c0 < cols) {
-#pragma unroll 4
-    for (int r = r_lo + rl; r < r_hi; r += 64) {
+#pragma unroll 8
+    for (int r = r_lo + rl; r < r_hi; r += 8) {
       float d[8];
-      unpack8(*reinterpret_cast<const uint4*>(dy + (long long)r * ld + c0), d);
+      unpack8(__ldcs(reinterpret_cast<const uint4*>(dy + (long long)r * ld + c0)), d);
       if (LN) {
         float xv[8];
-        unpack8(*reinterpret_cast<const uint4*>(x + (long long)r * cols + c0), xv);
-        const float mu = mean[r], rs = rstd[r];
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(x + (long long)r * cols + c0)), xv);
+        const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           a0[j] += d[j] * (xv[j] - mu) * rs;
@@ -206,12 +347,12 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
     if (LN) sh[NO - 1][rl][cv * 8 + j] = a1[j];
   }
   __syncthreads();
-  // reduce 64 row lanes: thread (k, c) for k < NO, c < 32
-  float part = 0.f;
-  const int k = threadIdx.x / 32, c = threadIdx.x % 32;
-  if (k < NO) {
-    for (int r = 0; r < 64; ++r) part += sh[k][r][c];
-    ws[((long long)split * NO + k) * cols + strip * 32 + c] = part;  // cols % 32 handled by host padding
+  for (int idx = threadIdx.x; idx < NO * CR_COLS; idx += 256) {
+    const int k = idx / CR_COLS, c = idx % CR_COLS;
+    float part = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) part += sh[k][r][c];
+    ws[((long long)split * NO + k) * ws_ld + strip * CR_COLS + c] = part;
   }
   __threadfence();
   __syncthreads();
@@ -219,14 +360,14 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (k < NO) {
-    float s = 0.f;
-    for (int sp = 0; sp < nsplit; ++sp) s += __ldcg(&ws[((long long)sp * NO + k) * cols + strip * 32 + c]);
-    const int col = strip * 32 + c;
-    if (col < cols) {
-      if (k == 0) out0[col] += s;
-      else out1[col] += s;
-    }
+  for (int idx = threadIdx.x; idx < NO * CR_COLS; idx += 256) {
+    const int k = idx / CR_COLS, c = idx % CR_COLS;
+    const int col = strip * CR_COLS + c;
+    if (col >= cols) continue;
+    float sum = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(&ws[((long long)sp * NO + k) * ws_ld + col]);
+    if (k == 0) out0[col] += sum;
+    else out1[col] += sum;
   }
   if (threadIdx.x == 0) tickets[strip] = 0;  // re-arm for the next launch (stream-ordered)
 }
@@ -424,6 +565,9 @@ static int grid_for(long long n, int per_block) {
 int kernels_preload() {
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)layernorm_fwd_kernel, (const void*)layernorm_bwd_dx_kernel,
+#define ZPP_PRE(H) (const void*)ln_fwd_warp_kernel<H>, (const void*)ln_bwd_dx_warp_kernel<H>,
+                       ZPP_LN_HV_LIST(ZPP_PRE)
+#undef ZPP_PRE
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_kernel,
                        (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel,
@@ -445,42 +589,46 @@ extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* b
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  layernorm_fwd_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
-                                                          (bf16*)y, mean, rstd, cols, eps);
+  if (!(cols % 256 == 0 && ln_warp_fwd(cols / 256, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y,
+                                      mean, rstd, rows, eps, STREAM(stream))))
+    layernorm_fwd_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
+                                                            (bf16*)y, mean, rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
 
 // workspace layout for the column reductions: [splits][2][cols_pad] floats + tickets
 extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) {
-  const int cols_pad = (cols + 31) / 32 * 32;
-  return (long long)CR_MAX_SPLIT * 2 * cols_pad + cols_pad / 32;
+  const int cols_pad = (cols + CR_COLS - 1) / CR_COLS * CR_COLS;
+  return (long long)CR_MAX_SPLIT * 2 * cols_pad + cols_pad / CR_COLS;
 }
 
 static int colred_launch(bool ln, const void* dy, long long ld, const void* x, const float* mean, const float* rstd,
                          float* out0, float* out1, float* ws, int rows, int cols, cudaStream_t st) {
-  const int strips = (cols + 31) / 32;
-  const int cols_pad = strips * 32;
+  const int strips = (cols + CR_COLS - 1) / CR_COLS;
+  const int cols_pad = strips * CR_COLS;
   const int splits = colred_splits(rows, strips);
   float* part = ws;
   unsigned* tickets = reinterpret_cast<unsigned*>(ws + (long long)CR_MAX_SPLIT * 2 * cols_pad);
   dim3 grid(strips, splits);
   if (ln)
     colred_kernel<true><<<grid, 256, 0, st>>>((const bf16*)dy, ld, (const bf16*)x, mean, rstd, out0, out1, part,
-                                              tickets, rows, cols_pad);
+                                              tickets, rows, cols, cols_pad);
   else
     colred_kernel<false><<<grid, 256, 0, st>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr, out0, nullptr, part,
-                                               tickets, rows, cols_pad);
+                                               tickets, rows, cols, cols_pad);
   return check_launch("colred");
 }
 
 extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                                  const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
                                  float* workspace, int rows, int cols, uintptr_t stream) {
-  if (cols % 32 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 32 != 0 or > 8192");
+  if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
-                                                             (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
+  if (!(cols % 256 == 0 && ln_warp_bwd(cols / 256, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
+                                      (const bf16*)dresid, (bf16*)dx, rows, STREAM(stream))))
+    layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
+                                                               (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc) return rc;
   return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, STREAM(stream));
@@ -488,7 +636,7 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
 
 extern "C" int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
                               uintptr_t stream) {
-  if (cols % 32 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols % 32 / ld % 8 != 0");
+  if (cols % 8 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols / ld % 8 != 0");
   if (!workspace) return set_error(ZPP_ERR_ARG, "colsum: workspace required");
   if (rows <= 0) return ZPP_OK;
   return colred_launch(false, dy, ld, nullptr, nullptr, nullptr, dbias, nullptr, workspace, rows, cols, STREAM(stream));

@@ -99,7 +99,7 @@ def test_gemm_f32_accumulate(M, N, K, cta_group):
     assert rel_err(C, ref) < 1e-5
 
 
-@pytest.mark.parametrize("cols", [256, 2048, 4096])
+@pytest.mark.parametrize("cols", [256, 2048, 4096, 5120, 1000 - 1000 % 8 + 8])
 def test_layernorm(cols):
     rows = 300
     x = bf(rows, cols, scale=2.0) + 0.5
