@@ -95,144 +95,6 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
   }
 }
 
-// Warp-per-row LayerNorm (h = 256 * HV): the row stays packed in registers (HV uint4 per
-// lane), every load/store instruction of a warp covers 512 contiguous bytes, and the
-// reductions are warp shuffles only (no block barriers), so many rows are in flight per SM.
-template <int HV>
-__global__ void __launch_bounds__(256, HV <= 12 ? 2 : 1) ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
-                                                          const bf16* __restrict__ b, bf16* __restrict__ y,
-                                                          float* __restrict__ mean_out, float* __restrict__ rstd_out,
-                                                          int rows, float eps) {
-  constexpr int COLS = HV * 256;
-  const int lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + (long long)row * COLS);
-    uint4 raw[HV];
-#pragma unroll
-    for (int i = 0; i < HV; ++i) raw[i] = __ldcs(xr + i * 32 + lane);
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < HV; ++i) {
-      float f[8];
-      unpack8(raw[i], f);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) s += f[j];
-    }
-    const float mu = warp_sum(s) * (1.f / COLS);
-    float q = 0.f;
-#pragma unroll
-    for (int i = 0; i < HV; ++i) {
-      float f[8];
-      unpack8(raw[i], f);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { const float d = f[j] - mu; q += d * d; }
-    }
-    const float rs = rsqrtf(warp_sum(q) * (1.f / COLS) + eps);
-    uint4* yr = reinterpret_cast<uint4*>(y + (long long)row * COLS);
-#pragma unroll 2
-    for (int i = 0; i < HV; ++i) {
-      float f[8], gg[8], bb[8], o[8];
-      unpack8(raw[i], f);
-      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i * 32 + lane), gg);
-      unpack8(__ldg(reinterpret_cast<const uint4*>(b) + i * 32 + lane), bb);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = (f[j] - mu) * rs * gg[j] + bb[j];
-      yr[i * 32 + lane] = pack8(o);
-    }
-    if (lane == 0) {
-      mean_out[row] = mu;
-      rstd_out[row] = rs;
-    }
-  }
-}
-
-template <int HV>
-__global__ void __launch_bounds__(256) ln_bwd_dx_warp_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                                             const float* __restrict__ mean,
-                                                             const float* __restrict__ rstd,
-                                                             const bf16* __restrict__ g,
-                                                             const bf16* __restrict__ dres, bf16* __restrict__ dx,
-                                                             int rows) {
-  constexpr int COLS = HV * 256;
-  const int lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + (long long)row * COLS);
-    const uint4* dr = reinterpret_cast<const uint4*>(dy + (long long)row * COLS);
-    uint4 rx[HV], rd[HV];
-#pragma unroll
-    for (int i = 0; i < HV; ++i) {
-      rx[i] = __ldg(xr + i * 32 + lane);
-      rd[i] = __ldg(dr + i * 32 + lane);
-    }
-    const float mu = mean[row], rs = rstd[row];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll 2
-    for (int i = 0; i < HV; ++i) {
-      float xv[8], dv[8], gg[8];
-      unpack8(rx[i], xv);
-      unpack8(rd[i], dv);
-      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i * 32 + lane), gg);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float dg = dv[j] * gg[j];
-        s1 += dg;
-        s2 += dg * (xv[j] - mu) * rs;
-      }
-    }
-    const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
-    uint4* o = reinterpret_cast<uint4*>(dx + (long long)row * COLS);
-    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (long long)row * COLS) : nullptr;
-#pragma unroll 2
-    for (int i = 0; i < HV; ++i) {
-      float xv[8], dv[8], gg[8], out[8];
-      unpack8(rx[i], xv);
-      unpack8(rd[i], dv);
-      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i * 32 + lane), gg);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) out[j] = rs * (dv[j] * gg[j] - m1 - (xv[j] - mu) * rs * m2);
-      if (rr) {
-        float rv[8];
-        unpack8(__ldcs(rr + i * 32 + lane), rv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) out[j] += rv[j];
-      }
-      o[i * 32 + lane] = pack8(out);
-    }
-  }
-}
-
-#define ZPP_LN_HV_LIST(X) X(1) X(2) X(4) X(8) X(12) X(16) X(20) X(24)
-
-static bool ln_warp_fwd(int hv, const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mu, float* rs, int rows,
-                        float eps, cudaStream_t st) {
-  const int grid = (rows + 7) / 8;
-  switch (hv) {
-#define ZPP_CASE(H) \
-  case H:           \
-    ln_fwd_warp_kernel<H><<<grid, 256, 0, st>>>(x, g, b, y, mu, rs, rows, eps); \
-    return true;
-    ZPP_LN_HV_LIST(ZPP_CASE)
-#undef ZPP_CASE
-    default:
-      return false;
-  }
-}
-
-static bool ln_warp_bwd(int hv, const bf16* dy, const bf16* x, const float* mu, const float* rs, const bf16* g,
-                        const bf16* dres, bf16* dx, int rows, cudaStream_t st) {
-  const int grid = (rows + 7) / 8;
-  switch (hv) {
-#define ZPP_CASE(H) \
-  case H:           \
-    ln_bwd_dx_warp_kernel<H><<<grid, 256, 0, st>>>(dy, x, mu, rs, g, dres, dx, rows); \
-    return true;
-    ZPP_LN_HV_LIST(ZPP_CASE)
-#undef ZPP_CASE
-    default:
-      return false;
-  }
-}
-
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
 // the two row sums fused into a single float2 block reduction.
 __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
@@ -565,9 +427,6 @@ static int grid_for(long long n, int per_block) {
 int kernels_preload() {
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)layernorm_fwd_kernel, (const void*)layernorm_bwd_dx_kernel,
-#define ZPP_PRE(H) (const void*)ln_fwd_warp_kernel<H>, (const void*)ln_bwd_dx_warp_kernel<H>,
-                       ZPP_LN_HV_LIST(ZPP_PRE)
-#undef ZPP_PRE
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_kernel,
                        (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel,
@@ -589,10 +448,8 @@ extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* b
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  if (!(cols % 256 == 0 && ln_warp_fwd(cols / 256, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y,
-                                      mean, rstd, rows, eps, STREAM(stream))))
-    layernorm_fwd_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
-                                                            (bf16*)y, mean, rstd, cols, eps);
+  layernorm_fwd_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
+                                                          (bf16*)y, mean, rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
 
@@ -625,10 +482,8 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  if (!(cols % 256 == 0 && ln_warp_bwd(cols / 256, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
-                                      (const bf16*)dresid, (bf16*)dx, rows, STREAM(stream))))
-    layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
-                                                               (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
+  layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
+                                                             (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc) return rc;
   return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, STREAM(stream));
