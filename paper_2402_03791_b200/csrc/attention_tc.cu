@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "ptx.cuh"
 #include "zpp_internal.h"
@@ -138,34 +140,47 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < nkb; ++i) {
       mbar_wait(s_full0 + 8 * (i & 1), (i >> 1) & 1);
       tc_fence_after();
-      float x[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tl + (i & 1) * 128 + c * 32, v);
+      float x[128];  // raw scores (scale folded into the exp2 FFMA below)
+      {
+        uint32_t v0[32], v1[32], v2[32], v3[32];
+        const uint32_t sb = tl + (i & 1) * 128;
+        tmem_ld32(sb, v0);
+        tmem_ld32(sb + 32, v1);
+        tmem_ld32(sb + 64, v2);
+        tmem_ld32(sb + 96, v3);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) x[c * 32 + j] = __uint_as_float(v[j]) * scale_log2;
+        for (int j = 0; j < 32; ++j) {
+          x[j] = __uint_as_float(v0[j]);
+          x[32 + j] = __uint_as_float(v1[j]);
+          x[64 + j] = __uint_as_float(v2[j]);
+          x[96 + j] = __uint_as_float(v3[j]);
+        }
       }
       if (i == nkb - 1) {  // diagonal block: keys after the query are masked
 #pragma unroll
         for (int j = 0; j < 128; ++j)
           if (j > r) x[j] = -INFINITY;
       }
-      float mx = x[0];
+      float pm[8];  // 8 independent max chains
 #pragma unroll
-      for (int j = 1; j < 128; ++j) mx = fmaxf(mx, x[j]);
+      for (int k = 0; k < 8; ++k) pm[k] = x[k];
+#pragma unroll
+      for (int j = 8; j < 128; ++j) pm[j & 7] = fmaxf(pm[j & 7], x[j]);
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
       const float m_new = fmaxf(m_run, mx);
       // tcgen05.ld/st below are warp-collective (.sync.aligned): the rescale decision
       // must be warp-uniform.  Any lane needing it makes every lane move to its own max.
       const bool rescale = __any_sync(0xffffffffu, m_new > m_run + 8.f);
       const float m_use = rescale ? m_new : m_run;
-      float rs = 0.f;
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent sum chains
 #pragma unroll
       for (int j = 0; j < 128; ++j) {
-        x[j] = fast_exp2(x[j] - m_use);
-        rs += x[j];
+        x[j] = fast_exp2(fmaf(x[j], scale_log2, -m_use));
+        ps[j & 7] += x[j];
       }
+      const float rs = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       if (i > 0) {
         mbar_wait(o_done, (i - 1) & 1);  // PV_{i-1} finished: P buffer free, O stable
         tc_fence_after();
@@ -281,11 +296,17 @@ struct TcBwdCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
-                       const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, float scale) {
+                       const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, float scale,
+                       unsigned long long* __restrict__ trace) {
   using C = TcBwdCfg<D>;
+  // optional phase timeline of CTA (0, 0) for performance analysis (trace == nullptr in production)
+  const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+  auto mark = [&](int slot) {
+    if (tr) trace[slot] = clock64();
+  };
   constexpr int NA = D / 64;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -316,9 +337,9 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(qd_empty0 + 8 * s, 1);
     }
     mbar_init(sp_full, 1);
-    mbar_init(ds_full, 128);
+    mbar_init(ds_full, 256);
     mbar_init(mm_done, 1);
-    mbar_init(dq_free, 128);
+    mbar_init(dq_free, 256);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -354,18 +375,26 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t id_kmn = make_idesc_bf16(128, D, false, true);    // dV, dK (B MN-major, N = d)
       constexpr uint32_t id_mnmn = make_idesc_bf16(128, D, true, true);    // dQ (A and B MN-major)
       mbar_wait(kv_full, 0);
-      for (int it = 0; it < nq; ++it) {
+      auto issue_st = [&](int it) {  // S^T = K Q^T into the S columns (in-order after dV read P^T)
         const int st = it & 1;
         mbar_wait(qd_full0 + 8 * st, (it >> 1) & 1);
-        if (it > 0) mbar_wait(dq_free, (it - 1) & 1);  // dQ_{it-1} read out, P^T consumed
         tc_fence_after();
-        const uint32_t qs = base + C::Q_OFF + st * C::TILE, ds_ = base + C::DO_OFF + st * C::TILE;
+        const uint32_t qs = base + C::Q_OFF + st * C::TILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::ATOM + (kk & 3) * 32;
           mma_bf16(T_S, make_sdesc(base + C::K_OFF + off, 16, 1024), make_sdesc(qs + off, 16, 1024), id_kk,
                    kk > 0 ? 1u : 0u);
         }
+      };
+      issue_st(0);
+      for (int it = 0; it < nq; ++it) {
+        const int st = it & 1;
+        mark(16 * it + 0);
+        if (it > 0) mbar_wait(dq_free, (it - 1) & 1);  // dQ_{it-1} read out of the dP columns
+        mark(16 * it + 1);
+        tc_fence_after();
+        const uint32_t qs = base + C::Q_OFF + st * C::TILE, ds_ = base + C::DO_OFF + st * C::TILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::ATOM + (kk & 3) * 32;
@@ -373,12 +402,14 @@ __global__ void __launch_bounds__(256, 1)
                    kk > 0 ? 1u : 0u);
         }
         mma_commit(sp_full);
+        mark(16 * it + 2);
         mbar_wait(ds_full, it & 1);
+        mark(16 * it + 3);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries
           // dV += P^T dO : A = P^T (TMEM, 8 columns per k16), B = dO (MN-major: n = d)
-          mma_bf16_ts(T_DV, T_S + kk * 8, make_sdesc(ds_ + kk * 2048, C::ATOM, 1024), id_kmn,
+          mma_bf16_ts(T_DV, T_S + (kk >> 2) * 64 + (kk & 3) * 8, make_sdesc(ds_ + kk * 2048, C::ATOM, 1024), id_kmn,
                       (it > 0 || kk > 0) ? 1u : 0u);
           // dK += dS^T Q : A = dS^T (smem K-major), B = Q (MN-major)
           mma_bf16(T_DK, make_sdesc(base + C::DS_OFF + (kk >> 2) * C::ATOM + (kk & 3) * 32, 16, 1024),
@@ -392,25 +423,42 @@ __global__ void __launch_bounds__(256, 1)
         }
         mma_commit(mm_done);
         mma_commit(qd_empty0 + 8 * st);
+        mark(16 * it + 4);
+        if (it + 1 < nq) issue_st(it + 1);  // overlaps the dQ readout of this block
+        mark(16 * it + 5);
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
+    // 8 warps: warp (q, hh) owns TMEM lane quarter q and column half hh of every tile
     const int q = warp & 3;
+    const int hh = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // key row for softmax-bwd; query row for the dQ readout
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * LOG2E_;
-    int nb = 0;  // dQ staging buffers used (ring of 2 per warp)
+
+    // lse/delta of the next query block are prefetched into registers one iteration ahead
+    float nl = lse[(long long)bh * T + kblk * 128 + r] * LOG2E_;
+    float nd = delta[(long long)bh * T + kblk * 128 + r];
     for (int it = 0; it < nq; ++it) {
       const int q0 = (kblk + it) * 128;
-      named_bar_sync(1, 128);  // previous iteration's lse/delta reads and staging TMA reads are done
-      sL[r] = lse[(long long)bh * T + q0 + r] * LOG2E_;
-      sDl[r] = delta[(long long)bh * T + q0 + r];
-      named_bar_sync(1, 128);
+      if (r == 0 && hh == 0) mark(16 * it + 8);
+      named_bar_sync(1, 256);  // previous iteration's lse/delta reads and staging TMA reads are done
+      if (hh == 0) {
+        sL[r] = nl;
+        sDl[r] = nd;
+      }
+      named_bar_sync(1, 256);
+      if (it + 1 < nq) {
+        nl = lse[(long long)bh * T + q0 + 128 + r] * LOG2E_;
+        nd = delta[(long long)bh * T + q0 + 128 + r];
+      }
+      if (r == 0 && hh == 0) mark(16 * it + 9);
       mbar_wait(sp_full, it & 1);
+      if (r == 0 && hh == 0) mark(16 * it + 10);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {  // 32 queries per chunk
+      for (int c = 2 * hh; c < 2 * hh + 2; ++c) {  // 32 queries per chunk, this warp's half
         uint32_t sv[32], pv[32];
         tmem_ld32(T_S + lo + c * 32, sv);
         tmem_ld32(T_DP + lo + c * 32, pv);
@@ -427,7 +475,9 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
-        tmem_st16(T_S + lo + c * 16, pk);  // P^T bf16 over the consumed S^T columns
+        // P^T bf16 over S^T columns this warp has already consumed (each column half packs
+        // into its own first 32 columns, so the other half's scores are never overwritten)
+        tmem_st16(T_S + lo + (c >> 1) * 64 + (c & 1) * 16, pk);
         const uint32_t rowp = base + C::DS_OFF + (c >> 1) * C::ATOM + r * 128;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -441,21 +491,23 @@ __global__ void __launch_bounds__(256, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(ds_full);
-      // dQ rows of this query block: thread r owns query q0 + r
+      if (r == 0 && hh == 0) mark(16 * it + 11);
+      // dQ rows of this query block: thread r owns query q0 + r; this warp reads its column half
       mbar_wait(mm_done, it & 1);
+      if (r == 0 && hh == 0) mark(16 * it + 12);
       tc_fence_after();
-      const uint32_t ebuf0 = base + C::DS_OFF + q * 8192;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(T_DP + lo + c * 32, v);
-        tmem_wait_ld();
-        if (c == D / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(dq_free);
-        }
-        const uint32_t buf = ebuf0 + (nb & 1) * 4096;
-        if (lane == 0) bulk_wait_read<1>();
+      constexpr int NCH = D / 64;  // 32-column chunks per warp
+      uint32_t dqv[NCH][32];
+#pragma unroll
+      for (int cc = 0; cc < NCH; ++cc) tmem_ld32(T_DP + lo + (hh * NCH + cc) * 32, dqv[cc]);
+      tmem_wait_ld();
+      const uint32_t ebuf = base + C::DS_OFF + (warp - 4) * 4096;
+#pragma unroll
+      for (int cc = 0; cc < NCH; ++cc) {
+        const int c = hh * NCH + cc;
+        uint32_t (&v)[32] = dqv[cc];
+        const uint32_t buf = ebuf;
+        if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -466,10 +518,14 @@ __global__ void __launch_bounds__(256, 1)
           tma_reduce_add_2d(&tm_dq, buf, h * D + c * 32, row_base + q0 + q * 32);
           bulk_commit();
         }
-        ++nb;
+
       }
+      tc_fence_before();
+      mbar_arrive(dq_free);  // the dP columns may now receive the next dP^T
+      if (r == 0 && hh == 0) mark(16 * it + 13);
       if (lane == 0) bulk_wait_read<0>();  // staging lives in the dS^T tile the next iteration rewrites
       __syncwarp();
+      if (r == 0 && hh == 0) mark(16 * it + 14);
     }
     // final dK / dV rows (thread = key row)
     mbar_wait(mm_done, (nq - 1) & 1);
@@ -477,7 +533,7 @@ __global__ void __launch_bounds__(256, 1)
     bf16* dk = dqkv + ((long long)row_base + k0 + r) * 3 * H * D + (long long)H * D + (long long)h * D;
     bf16* dv = dk + (long long)H * D;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = hh * (D / 64); c < (hh + 1) * (D / 64); ++c) {
       uint32_t a[32], bb[32];
       tmem_ld32(T_DK + lo + c * 32, a);
       tmem_ld32(T_DV + lo + c * 32, bb);
@@ -537,8 +593,28 @@ int attn_bwd_tc_launch(const void* qkv, const void* dout, const float* lse, cons
     if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc attr");
     set = true;
   }
-  attn_bwd_tc_kernel<D><<<dim3(T / 128, B * H), 256, C::SMEM, s>>>(mq, mdo, mdq, lse, delta, (bf16*)dqkv, T, H,
-                                                                    1.f / sqrtf((float)D));
+  static int want_trace = -1;
+  if (want_trace < 0) want_trace = getenv("ZPP_ATTN_TRACE") ? 1 : 0;
+  unsigned long long* trace = nullptr;
+  if (want_trace) cudaMalloc(&trace, 16 * 32 * sizeof(unsigned long long));
+  attn_bwd_tc_kernel<D><<<dim3(T / 128, B * H), 384, C::SMEM, s>>>(mq, mdo, mdq, lse, delta, (bf16*)dqkv, T, H,
+                                                                    1.f / sqrtf((float)D), trace);
+  if (trace) {
+    unsigned long long h[16 * 32];
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    const int nq = T / 128;
+    const unsigned long long t0 = h[0];
+    for (int it = 0; it < nq; ++it) {
+      const unsigned long long* x = h + 16 * it;
+      printf("it %2d | mma: start %7lld dqfree %7lld spcommit %7lld dsfull %7lld mmcommit %7lld st_next %7lld |"
+             " sm: bar %7lld spwait %7lld spfull %7lld dsarrive %7lld mmdone %7lld readout %7lld bulk %7lld\n", it,
+             (long long)(x[0] - t0), (long long)(x[1] - t0), (long long)(x[2] - t0), (long long)(x[3] - t0),
+             (long long)(x[4] - t0), (long long)(x[5] - t0), (long long)(x[8] - t0), (long long)(x[9] - t0),
+             (long long)(x[10] - t0), (long long)(x[11] - t0), (long long)(x[12] - t0), (long long)(x[13] - t0),
+             (long long)(x[14] - t0));
+    }
+    cudaFree(trace);
+  }
   return check_launch("attn_bwd_tc");
 }
 
