@@ -74,18 +74,19 @@ long long zpp_attn_bwd_workspace_floats(int batch, int seq, int heads, int head_
 /* ---- LayerNorm (fp32 statistics) ---------------------------------------------- */
 int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                       int rows, int cols, float eps, uintptr_t stream);
-/* dx = LNbwd(dy) (+ dresid); dgamma/dbeta (fp32) += column sums (deterministic).
+/* dx = LNbwd(dy) (+ dresid); dgamma/dbeta (fp32) += column sums (deterministic), or = when
+ * accumulate == 0 (the first writer of a gradient in an accumulation window).
  * workspace: zpp_layernorm_bwd_workspace_floats() floats, zero-initialised once (it holds
  * self-re-arming tickets); reusable by later calls on the same stream.  cols % 32 == 0. */
 int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const void* gamma,
                       const void* dresid, void* dx, float* dgamma, float* dbeta, float* workspace, int rows,
-                      int cols, uintptr_t stream);
+                      int cols, int accumulate, uintptr_t stream);
 long long zpp_layernorm_bwd_workspace_floats(int rows, int cols);
 
-/* ---- bias gradient: dbias(f32)[c] += sum_r dy[r,c] (deterministic); workspace as for
+/* ---- bias gradient: dbias(f32)[c] += sum_r dy[r,c] (deterministic; = when accumulate == 0); workspace as for
  * zpp_layernorm_bwd (zero-initialised once, zpp_layernorm_bwd_workspace_floats(rows, cols)). */
 int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
-                   uintptr_t stream);
+                   int accumulate, uintptr_t stream);
 
 /* ---- elementwise -------------------------------------------------------------- */
 int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream);

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
                                                      const float* __restrict__ rstd, float* __restrict__ out0,
                                                      float* __restrict__ out1, float* __restrict__ ws,
                                                      unsigned* __restrict__ tickets, int rows, int cols,
-                                                     int ws_ld) {
+                                                     int ws_ld, int accumulate) {
   constexpr int NO = LN ? 2 : 1;
   __shared__ float sh[NO][8][CR_COLS + 4];
   __shared__ unsigned last;
@@ -228,8 +228,8 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
     if (col >= cols) continue;
     float sum = 0.f;
     for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(&ws[((long long)sp * NO + k) * ws_ld + col]);
-    if (k == 0) out0[col] += sum;
-    else out1[col] += sum;
+    float* o = k == 0 ? out0 : out1;
+    o[col] = accumulate ? o[col] + sum : sum;
   }
   if (threadIdx.x == 0) tickets[strip] = 0;  // re-arm for the next launch (stream-ordered)
 }
@@ -460,7 +460,7 @@ extern "C" long long zpp_layernorm_bwd_workspace_floats(int rows, int cols) {
 }
 
 static int colred_launch(bool ln, const void* dy, long long ld, const void* x, const float* mean, const float* rstd,
-                         float* out0, float* out1, float* ws, int rows, int cols, cudaStream_t st) {
+                         float* out0, float* out1, float* ws, int rows, int cols, int accumulate, cudaStream_t st) {
   const int strips = (cols + CR_COLS - 1) / CR_COLS;
   const int cols_pad = strips * CR_COLS;
   const int splits = colred_splits(rows, strips);
@@ -469,16 +469,16 @@ static int colred_launch(bool ln, const void* dy, long long ld, const void* x, c
   dim3 grid(strips, splits);
   if (ln)
     colred_kernel<true><<<grid, 256, 0, st>>>((const bf16*)dy, ld, (const bf16*)x, mean, rstd, out0, out1, part,
-                                              tickets, rows, cols, cols_pad);
+                                              tickets, rows, cols, cols_pad, accumulate);
   else
     colred_kernel<false><<<grid, 256, 0, st>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr, out0, nullptr, part,
-                                               tickets, rows, cols, cols_pad);
+                                               tickets, rows, cols, cols_pad, accumulate);
   return check_launch("colred");
 }
 
 extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                                  const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
-                                 float* workspace, int rows, int cols, uintptr_t stream) {
+                                 float* workspace, int rows, int cols, int accumulate, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
@@ -486,15 +486,17 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
                                                              (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc) return rc;
-  return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, STREAM(stream));
+  return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, accumulate,
+                       STREAM(stream));
 }
 
 extern "C" int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,
-                              uintptr_t stream) {
+                              int accumulate, uintptr_t stream) {
   if (cols % 8 || ld % 8) return set_error(ZPP_ERR_ARG, "colsum: cols / ld % 8 != 0");
   if (!workspace) return set_error(ZPP_ERR_ARG, "colsum: workspace required");
   if (rows <= 0) return ZPP_OK;
-  return colred_launch(false, dy, ld, nullptr, nullptr, nullptr, dbias, nullptr, workspace, rows, cols, STREAM(stream));
+  return colred_launch(false, dy, ld, nullptr, nullptr, nullptr, dbias, nullptr, workspace, rows, cols, accumulate,
+                       STREAM(stream));
 }
 
 extern "C" int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream) {

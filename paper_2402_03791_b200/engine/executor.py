@@ -74,6 +74,25 @@ class _Stage:
             self.g[key] = self.grad_full[s.offset:s.offset + s.numel].view(*s.shape)
         self.ag_event = None        # compute must wait before using gathered params
         self.grad_free_event = None  # compute must wait before writing grad_full again
+        # Gradients are never memset: the first writer of each tensor in an accumulation
+        # window (a step at D == 1, one unit's reduce-scatter at D > 1) stores instead of
+        # accumulating.  Only the embedding grads (row scatter-add) are zeroed.
+        self.scatter_keys = [k for k in self.g if k[0] in ("wte", "wpe")]
+        self.new_window()
+
+    def new_window(self) -> None:
+        self.fresh = set(self.g).difference(self.scatter_keys)
+
+    def accumulate(self, key) -> bool:
+        """False exactly once per window for ``key``: that writer overwrites."""
+        if key in self.fresh:
+            self.fresh.discard(key)
+            return False
+        return True
+
+    def zero_scatter_grads(self, stream) -> None:
+        for k in self.scatter_keys:
+            ops.zero(self.g[k], stream=stream)
 
 
 class Runtime:
@@ -306,7 +325,8 @@ class Runtime:
         n, ns = st.lay.numel, st.lay.shard_numel
         send, recv = self.rs_send[:n], self.rs_recv[:ns]
         ops.cast_scale(st.grad_full, send, 1.0, stream=rs)
-        ops.zero(st.grad_full, stream=rs)
+        st.zero_scatter_grads(rs)
+        st.new_window()
         st.grad_free_event = self._record(rs)
         lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], send.data_ptr(), recv.data_ptr(), ns, 0,
                  rs.cuda_stream)
@@ -323,7 +343,11 @@ class Runtime:
         if self.capture_grads:
             self.captured = {s: st.grad_shard.clone() for s, st in self.stages.items()}
         for st in self.stages.values():
-            ops.zero(st.grad_shard, stream=self.s_comp)
+            if self.D > 1:
+                ops.zero(st.grad_shard, stream=self.s_comp)  # reduce-scatter results accumulate here
+            else:
+                st.zero_scatter_grads(self.s_comp)
+                st.new_window()
         self.opt_event = self._record(self.s_comp)
 
     capture_grads = False
@@ -448,7 +472,8 @@ class Runtime:
             ops.gemm(stash["dlogits"], P[("w_lm", None)], dxf, b_t=True)
             dx = e(T, h)
             ops.layernorm_bwd(dxf, stash["xlast"], stash["muf"], stash["rf"], P[("lnf_g", None)], dx,
-                              G[("lnf_g", None)], G[("lnf_b", None)], self.ln_ws)
+                              G[("lnf_g", None)], G[("lnf_b", None)], self.ln_ws,
+                              accumulate=st.accumulate(("lnf_g", None)) | st.accumulate(("lnf_b", None)))
             del stash["xlast"], stash["muf"], stash["rf"]
         elif self._dev_of(s + 1) == self.p:
             dx = self._local_grad.pop((s, m))
@@ -464,7 +489,8 @@ class Runtime:
             ops.gemm(du, P[("w_fc1", l)], dxn2, b_t=True)
             dx1 = e(T, h)
             ops.layernorm_bwd(dxn2, a["x1"], a["mu2"], a["r2"], P[("ln2_g", l)], dx1, G[("ln2_g", l)],
-                              G[("ln2_b", l)], self.ln_ws, dresid=d2)
+                              G[("ln2_b", l)], self.ln_ws, dresid=d2,
+                              accumulate=st.accumulate(("ln2_g", l)) | st.accumulate(("ln2_b", l)))
             do = e(T, h)
             ops.gemm(dx1, P[("w_proj", l)], do, b_t=True)
             dqkv = e(T, 3 * h)
@@ -473,7 +499,8 @@ class Runtime:
             ops.gemm(dqkv, P[("w_qkv", l)], dxn1, b_t=True)
             dxl = e(T, h)
             ops.layernorm_bwd(dxn1, a["x"], a["mu1"], a["r1"], P[("ln1_g", l)], dxl, G[("ln1_g", l)],
-                              G[("ln1_b", l)], self.ln_ws, dresid=dx1)
+                              G[("ln1_b", l)], self.ln_ws, dresid=dx1,
+                              accumulate=st.accumulate(("ln1_g", l)) | st.accumulate(("ln1_b", l)))
             # keep only what W needs: inputs of the linears and their output grads
             stash["layers"][i] = {"xn1": a["xn1"], "o": a["o"], "xn2": a["xn2"], "g": a["g"],
                                   "d2": d2, "du": du, "dx1": dx1, "dqkv": dqkv}
@@ -495,11 +522,12 @@ class Runtime:
             a = stash["layers"][i]
             for dy, x, w, bias in (("d2", "g", "w_fc2", "b_fc2"), ("du", "xn2", "w_fc1", "b_fc1"),
                                    ("dx1", "o", "w_proj", "b_proj"), ("dqkv", "xn1", "w_qkv", "b_qkv")):
-                ops.gemm(a[dy], a[x], G[(w, l)], a_t=True, b_t=True, epilogue=ops.EPI_F32_ACC)
-                ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws)
+                ops.gemm(a[dy], a[x], G[(w, l)], a_t=True, b_t=True,
+                         epilogue=ops.EPI_F32_ACC if st.accumulate((w, l)) else ops.EPI_F32)
+                ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws, accumulate=st.accumulate((bias, l)))
         if s == self.S - 1:
             ops.gemm(stash["dlogits"], stash["xf"], G[("w_lm", None)], a_t=True, b_t=True,
-                     epilogue=ops.EPI_F32_ACC)
+                     epilogue=ops.EPI_F32_ACC if st.accumulate(("w_lm", None)) else ops.EPI_F32)
         if s == 0:
             ops.embed_bwd(self._ids[m], stash["demb"], G[("wte", None)], G[("wpe", None)],
                           self.spec.seq_len)

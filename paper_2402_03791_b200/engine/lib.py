@@ -30,9 +30,9 @@ _SIGS = {
     "zpp_attn_bwd": (c_int, [P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_stream]),
     "zpp_attn_bwd_workspace_floats": (c_longlong, [c_int, c_int, c_int, c_int]),
     "zpp_layernorm_fwd": (c_int, [P, P, P, P, P, P, c_int, c_int, c_float, c_stream]),
-    "zpp_layernorm_bwd": (c_int, [P, P, P, P, P, P, P, P, P, P, c_int, c_int, c_stream]),
+    "zpp_layernorm_bwd": (c_int, [P, P, P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_layernorm_bwd_workspace_floats": (c_longlong, [c_int, c_int]),
-    "zpp_colsum_acc": (c_int, [P, c_size, P, P, c_int, c_int, c_stream]),
+    "zpp_colsum_acc": (c_int, [P, c_size, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_gelu_fwd": (c_int, [P, P, c_size, c_stream]),
     "zpp_embed_fwd": (c_int, [P, P, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_embed_bwd": (c_int, [P, P, P, P, c_int, c_int, c_int, c_stream]),

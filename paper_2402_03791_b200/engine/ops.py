@@ -102,17 +102,20 @@ def layernorm_bwd_workspace(rows: int, cols: int) -> int:
     return lib.load().zpp_layernorm_bwd_workspace_floats(rows, cols)
 
 
-def layernorm_bwd(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, workspace, dresid=None, stream=None):
+def layernorm_bwd(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, workspace, dresid=None, accumulate=True,
+                  stream=None):
+    """dgamma/dbeta += column sums, or = when ``accumulate`` is False (first writer)."""
     rows, cols = x.shape
     _count(2)
     lib.call("zpp_layernorm_bwd", _p(dy), _p(x), _p(mean), _p(rstd), _p(gamma), _p(dresid), _p(dx),
-             _p(dgamma), _p(dbeta), _p(workspace), rows, cols, _s(stream))
+             _p(dgamma), _p(dbeta), _p(workspace), rows, cols, int(accumulate), _s(stream))
 
 
-def colsum_acc(dy, dbias, workspace, stream=None):
+def colsum_acc(dy, dbias, workspace, accumulate=True, stream=None):
     rows, cols = dy.shape
-    _count(2)
-    lib.call("zpp_colsum_acc", _p(dy), _ld(dy), _p(dbias), _p(workspace), rows, cols, _s(stream))
+    _count(1)
+    lib.call("zpp_colsum_acc", _p(dy), _ld(dy), _p(dbias), _p(workspace), rows, cols, int(accumulate),
+             _s(stream))
 
 
 def colsum_workspace(rows: int, cols: int) -> int:

@@ -124,6 +124,11 @@ def test_layernorm(cols):
     assert rel_err(dx, xf.grad + dres.float()) < 1e-2
     assert rel_err(dg, gf.grad) < 1e-4
     assert rel_err(db, bff.grad) < 1e-4
+    dg.fill_(123.0)
+    db.fill_(-7.0)
+    ops.layernorm_bwd(dy, x, mean, rstd, g, dx, dg, db, ws, dresid=dres, accumulate=False)  # overwrite
+    assert rel_err(dg, gf.grad) < 1e-4
+    assert rel_err(db, bff.grad) < 1e-4
 
 
 @pytest.mark.parametrize("rows,cols", [(1000, 768), (2048, 16384), (64, 96)])
@@ -136,6 +141,8 @@ def test_colsum(rows, cols):
     assert rel_err(acc, ref) < 1e-5
     ops.colsum_acc(dy, acc, ws)  # tickets re-armed: a second launch accumulates again
     assert rel_err(acc, ref + dy.float().sum(0)) < 1e-5
+    ops.colsum_acc(dy, acc, ws, accumulate=False)  # first writer of a window overwrites
+    assert rel_err(acc, dy.float().sum(0)) < 1e-5
 
 
 def _attn_ref(qkv, b, s, H, D):
