@@ -23,6 +23,15 @@
 //   warps 4-7  epilogue: tcgen05.ld -> bias/GeLU/dGeLU/residual/cast -> swizzled
 //              per-warp smem staging -> TMA store (bf16/fp32) or TMA reduce-add
 //              (fp32 +=, so the gradient accumulation never round-trips the SM).
+//
+// Hybrid data-parallel + stream-K work list (wave quantisation): with U persistent units
+// and T tiles, the floor(T/U)*U "full-wave" tiles are whole work items; the T mod U
+// remainder tiles are split into p k-ranges ("pieces") so the last wave is p times
+// finer.  A piece that finds the other p-1 already arrived (per-(tile, warp) counter)
+// finalises the tile; otherwise it parks its fp32 partial in a per-stream workspace and
+// bumps the counter -- and if that bump was the last, it finalises after all.  Nobody
+// waits, and the finaliser sums the pieces in piece order (deterministic).  E.g. M=2048 x N=4096 at 74 SM pairs: 128 tiles = 1.73 waves
+// -> 74 whole tiles + 54 tiles x 4 pieces = 1.75 tile-times instead of 2.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -48,6 +57,22 @@ struct EpiParams {
   int mode;
   int M, N;
 };
+
+// Stream-K split of the work list (see header).  No split: dp_tiles = tiles, pieces = 1.
+struct SkParams {
+  int dp_tiles;
+  int pieces;
+  float* ws;        // [(sk_tile * pieces + piece)][BN/32][TILE_M/32][8][32 lanes] float4 partials
+  unsigned* flags;  // [sk_tile][CG][4 epilogue warps] arrival counters, re-armed by the finisher
+  unsigned long long* trace;  // ZPP_GEMM_TRACE: [cta][GEMM_TRACE_ITEMS][6] globaltimer stamps, or null
+};
+constexpr int GEMM_TRACE_ITEMS = 32;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int BN, int CG>
 struct GemmCfg {
@@ -147,7 +172,7 @@ template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, int M, int N, int K, EpiParams ep,
-                        unsigned* __restrict__ sched) {
+                        SkParams sk, unsigned* __restrict__ sched) {
   using Cfg = GemmCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int TILE_M = GEMM_BM * CG;
@@ -214,6 +239,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_tiles = num_m * num_n;
   const int num_k = (K + GEMM_BK - 1) / GEMM_BK;
   const bool n_fast = M > N;
+  const int num_items = sk.dp_tiles + (num_tiles - sk.dp_tiles) * sk.pieces;
+  // work item -> (tile, k-block range, stream-K tile index or -1, piece)
+  auto decode = [&](int item, int& tile, int& kb0, int& kb1, int& skt, int& piece) {
+    if (item < sk.dp_tiles) {
+      tile = item; kb0 = 0; kb1 = num_k; skt = -1; piece = 0;
+    } else {
+      const int j = item - sk.dp_tiles;
+      skt = j / sk.pieces;
+      piece = j - skt * sk.pieces;
+      tile = sk.dp_tiles + skt;
+      kb0 = piece * num_k / sk.pieces;
+      kb1 = (piece + 1) * num_k / sk.pieces;
+    }
+  };
   // Readers take the next tile id from the ring (leader's ring_empty counts the readers).
   const uint32_t ring_empty_leader = (CG == 2) ? map_cta(ring_empty(0), 0) : ring_empty(0);
   auto next_tile = [&](int it, bool arrive) -> int {
@@ -247,12 +286,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         } else {
           tile = next_tile(it, true);
         }
-        if (tile >= num_tiles) break;
+        if (tile >= num_items) break;
+        int kb0, kb1, skt, piece;
+        decode(tile, tile, kb0, kb1, skt, piece);
         int mt, nt;
         tile_coords(tile, num_m, num_n, n_fast, mt, nt);
         const int m0 = mt * TILE_M + crank * GEMM_BM;
         const int n0 = nt * BN + crank * BNL;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t fb = full_bar(stage);
           if (leader) mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES * CG);
@@ -290,14 +331,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
-        const int tile = next_tile(it, true);
-        if (tile >= num_tiles) break;
+        const int item = next_tile(it, true);
+        if (item >= num_items) break;
+        int tile, kb0, kb1, skt, piece;
+        decode(item, tile, kb0, kb1, skt, piece);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         tc_fence_after();
+        unsigned long long* tr = (sk.trace && it < GEMM_TRACE_ITEMS)
+                                     ? sk.trace + ((size_t)blockIdx.x * GEMM_TRACE_ITEMS + it) * 6 : nullptr;
+        if (tr) { tr[0] = item; tr[1] = gtimer(); }
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           const uint32_t a_s = sA + stage * Cfg::A_BYTES;
@@ -306,8 +352,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = make_sdesc(a_s + k * A_KSTEP, A_LBO, 1024);
             const uint64_t bd = make_sdesc(b_s + k * B_KSTEP, B_LBO, 1024);
-            if (CG == 2) mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
-            else mma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+            if (CG == 2) mma_bf16_2sm(d_tmem, ad, bd, idesc, accum);
+            else mma_bf16(d_tmem, ad, bd, idesc, accum);
           }
           if (CG == 2) mma_commit_2sm(empty_bar(stage), 0x3);
           else mma_commit(empty_bar(stage));
@@ -315,6 +362,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         if (CG == 2) mma_commit_2sm(tfull_bar(acc), 0x3);
         else mma_commit(tfull_bar(acc));
+        if (tr) tr[2] = gtimer();
       }
     }
     __syncwarp();
@@ -326,21 +374,74 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tempty_leader = (CG == 2) ? map_cta(tempty_bar(0), 0) : tempty_bar(0);
     int nb = 0;  // nb: staging buffers used so far (ring of 2)
     for (int it = 0;; ++it) {
-      const int tile = next_tile(it, false);
+      const int item = next_tile(it, false);
       __syncwarp();
       if (lane == 0) {
         if (CG == 2) mbar_arrive_remote(ring_empty_leader + 8u * (it % RING));
         else mbar_arrive(ring_empty(it % RING));
       }
-      if (tile >= num_tiles) break;
+      if (item >= num_items) break;
+      int tile, kb0, kb1, skt, piece;
+      decode(item, tile, kb0, kb1, skt, piece);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int rl = crank * GEMM_BM + q * 32 + lane;  // row within the TILE_M tile
+      unsigned long long* etr = (sk.trace && it < GEMM_TRACE_ITEMS && q == 0 && lane == 0)
+                                    ? sk.trace + ((size_t)blockIdx.x * GEMM_TRACE_ITEMS + it) * 6 : nullptr;
+      if (etr) { if (!leader || CG == 1) etr[0] = item; etr[3] = gtimer(); }
+      // stream-K item: the LAST piece of a tile to arrive finalises it; the others park
+      // their fp32 partial in the workspace.  Nobody waits.
+      bool own_in_ws = false;  // finisher whose own partial already went to the workspace
+      if (skt >= 0) {
+        unsigned* f = sk.flags + (skt * CG + crank) * 4 + q;
+        uint32_t seen = 0;
+        if (lane == 0) seen = ld_acquire_gpu_u32(f);
+        seen = __shfl_sync(0xffffffffu, seen, 0);
+        if (seen != static_cast<uint32_t>(sk.pieces - 1)) {
+          mbar_wait(tfull_bar(acc), acc_phase);
+          tc_fence_after();
+          if (etr) etr[4] = gtimer();
+          const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+          float* dst = sk.ws + (static_cast<long long>(skt) * sk.pieces + piece) * (TILE_M * BN);
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(t_row + c, v);
+            tmem_wait_ld();
+            if (c + 32 >= BN) {
+              tc_fence_before();
+              if (CG == 2) mbar_arrive_remote(tempty_leader + 8u * acc);
+              else mbar_arrive(tempty_bar(acc));
+            }
+            // lane-contiguous: float4 j of every lane is one 512-byte run (coalesced)
+            float4* d4 = reinterpret_cast<float4*>(dst) + ((c / 32) * (TILE_M / 32) + (rl >> 5)) * 256 + lane;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              __stcg(d4 + 32 * j, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                         __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+          }
+          __threadfence();
+          __syncwarp();
+          uint32_t prev = 0;
+          if (lane == 0) prev = atomicAdd(f, 1u);
+          prev = __shfl_sync(0xffffffffu, prev, 0);
+          if (etr) etr[5] = gtimer() | (1ull << 63);  // partial parked
+          if (prev != static_cast<uint32_t>(sk.pieces - 1)) continue;  // a later piece finalises
+          own_in_ws = true;
+        }
+        __threadfence();  // acquire: every other piece's partial is visible
+        if (lane == 0) *f = 0;  // re-arm (the next launch on this stream is ordered after this one)
+      }
+      const bool finisher = skt >= 0;
       int mt, nt;
       tile_coords(tile, num_m, num_n, n_fast, mt, nt);
       const int row0 = mt * TILE_M + crank * GEMM_BM + q * 32;
       const int n0 = nt * BN;
-      mbar_wait(tfull_bar(acc), acc_phase);
-      tc_fence_after();
+      if (!own_in_ws) {
+        mbar_wait(tfull_bar(acc), acc_phase);
+        tc_fence_after();
+      }
+      if (etr) etr[4] = gtimer();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int row = row0 + lane;
       constexpr int CHUNK = 32;
@@ -351,7 +452,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int nsub = cols_per_store / CHUNK;
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
-          if (sub < nsub) {
+          if (sub < nsub && !own_in_ws) {
             uint32_t v[32];
             tmem_ld32(t_row + c + sub * CHUNK, v);
             tmem_wait_ld();
@@ -359,7 +460,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int j = 0; j < 32; ++j) x[sub][j] = __uint_as_float(v[j]);
           }
         }
-        if (c + cols_per_store >= BN) {  // accumulator fully in registers: release TMEM early
+        if (finisher) {  // sum all pieces in piece order (deterministic whoever finalises)
+          float y[2][32];
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) y[sub][j] = 0.f;
+#pragma unroll 1
+          for (int pc = 0; pc < sk.pieces; ++pc) {
+            if (pc == piece && !own_in_ws) {
+#pragma unroll
+              for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[sub][j] += x[sub][j];
+              continue;
+            }
+            const float* src = sk.ws + (static_cast<long long>(skt) * sk.pieces + pc) * (TILE_M * BN);
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+              if (sub < nsub) {
+                const float4* s4 = reinterpret_cast<const float4*>(src) +
+                                   (((c + sub * CHUNK) / 32) * (TILE_M / 32) + (rl >> 5)) * 256 + lane;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float4 t = __ldcg(s4 + 32 * j);
+                  y[sub][4 * j] += t.x; y[sub][4 * j + 1] += t.y; y[sub][4 * j + 2] += t.z; y[sub][4 * j + 3] += t.w;
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[sub][j] = y[sub][j];
+        }
+        if (c + cols_per_store >= BN && !own_in_ws) {  // accumulator in registers: release TMEM early
           tc_fence_before();
           if (CG == 2) mbar_arrive_remote(tempty_leader + 8u * acc);
           else mbar_arrive(tempty_bar(acc));
@@ -398,6 +533,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         ++nb;
       }
+      if (etr) etr[5] = gtimer();
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
@@ -446,6 +582,106 @@ static unsigned* sched_slot() {
     cudaDeviceSynchronize();
   }
   return buf + 2 * (next++ % NSLOT);
+}
+
+// Stream-K workspaces: one per stream that launches split GEMMs (launches on one stream
+// are ordered, so they can share it).  Allocated at preload time -- never inside a step,
+// where an allocation could wait on spinning NCCL kernels.  A launch on a stream beyond
+// the table simply runs without the split.
+constexpr int SK_MAX_PIECES = 4;
+constexpr int SK_CTX = 2;
+constexpr long long SK_WS_FLOATS = 148LL * SK_MAX_PIECES * 128 * 256;  // (units-1)*p*tile, both CGs
+constexpr int SK_FLAGS = 148 * 4;
+struct SkCtx {
+  cudaStream_t stream;
+  bool used;
+  float* ws;
+  unsigned* flags;
+};
+static SkCtx g_sk[SK_CTX];
+static unsigned long long* g_gemm_trace = nullptr;  // ZPP_GEMM_TRACE=1: last launch's timeline
+static bool g_sk_ready = false;
+static int g_sk_mode = -1;  // ZPP_GEMM_STREAMK: 0 off, 1 on (default)
+
+static int sk_alloc() {
+  if (g_sk_ready) return ZPP_OK;
+  for (auto& c : g_sk) {
+    if (cudaMalloc(&c.ws, SK_WS_FLOATS * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&c.flags, SK_FLAGS * sizeof(unsigned)) != cudaSuccess)
+      return set_error(ZPP_ERR_CUDA, "gemm: stream-K workspace allocation failed");
+    if (cudaMemset(c.flags, 0, SK_FLAGS * sizeof(unsigned)) != cudaSuccess)
+      return set_error(ZPP_ERR_CUDA, "gemm: stream-K flag init failed");
+    c.used = false;
+  }
+  const char* tr = getenv("ZPP_GEMM_TRACE");
+  if (tr && atoi(tr) && !g_gemm_trace) {
+    const size_t bytes = 148ull * GEMM_TRACE_ITEMS * 6 * sizeof(unsigned long long);
+    if (cudaMalloc(&g_gemm_trace, bytes) != cudaSuccess) return set_error(ZPP_ERR_CUDA, "gemm trace alloc");
+    cudaMemset(g_gemm_trace, 0, bytes);
+  }
+  cudaDeviceSynchronize();
+  g_sk_ready = true;
+  return ZPP_OK;
+}
+
+static SkCtx* sk_ctx(cudaStream_t s) {
+  if (!g_sk_ready) return nullptr;
+  for (auto& c : g_sk)
+    if (c.used && c.stream == s) return &c;
+  for (auto& c : g_sk)
+    if (!c.used) {
+      c.used = true;
+      c.stream = s;
+      return &c;
+    }
+  return nullptr;
+}
+
+// Choose the split: whole tiles for the full waves, p pieces for the remainder, p
+// minimising (k-blocks on the critical path + a per-piece overhead for the partial
+// round trip and pipeline refill).
+static SkParams sk_plan(int tiles, int units, int num_k, int tile_m, int bn, cudaStream_t s) {
+  SkParams sk{tiles, 1, nullptr, nullptr, g_gemm_trace};
+  if (g_sk_mode < 0) {
+    const char* e = getenv("ZPP_GEMM_STREAMK");
+    g_sk_mode = e ? atoi(e) : 1;
+  }
+  if (!g_sk_mode || tiles <= units || tiles % units == 0) return sk;
+  const int full = tiles / units, r = tiles % units;
+  static int force = -1;  // ZPP_GEMM_SK_FORCE=p: tuning override of the piece count
+  if (force < 0) {
+    const char* e = getenv("ZPP_GEMM_SK_FORCE");
+    force = e ? atoi(e) : 0;
+  }
+  if (force > 0 && force <= SK_MAX_PIECES) {
+    SkCtx* c = sk_ctx(s);
+    if (!c) return sk;
+    sk.dp_tiles = full * units;
+    sk.pieces = force;
+    sk.ws = c->ws;
+    sk.flags = c->flags;
+    return sk;
+  }
+  // Measured (tools/gemm_trace.py): parking a 128 KB partial ~6 us and summing it back
+  // ~7 us per piece -- the read-back is latency-bound at ~32 KB in flight per SM -- so one
+  // extra piece costs ~22 k-blocks (0.34 us each at 256x256 pair tiles).
+  constexpr int OVH_KB = 22;
+  long long best = (long long)(full + 1) * num_k;
+  int best_p = 1;
+  for (int p = 2; p <= SK_MAX_PIECES; ++p) {
+    if (num_k < 4 * p) break;
+    const int waves = (r * p + units - 1) / units;
+    const long long cost = (long long)full * num_k + (long long)waves * ((num_k + p - 1) / p) + OVH_KB * (p - 1);
+    if (cost < best) { best = cost; best_p = p; }
+  }
+  if (best_p == 1) return sk;
+  SkCtx* c = sk_ctx(s);
+  if (!c || (long long)r * best_p * tile_m * bn > SK_WS_FLOATS) return sk;
+  sk.dp_tiles = full * units;
+  sk.pieces = best_p;
+  sk.ws = c->ws;
+  sk.flags = c->flags;
+  return sk;
 }
 
 template <int BN, bool A_MN, bool B_MN, int CG>
@@ -497,7 +733,8 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
   cfg.numAttrs = 1;
   unsigned* sched = sched_slot();
   if (!sched) return set_error(ZPP_ERR_CUDA, "gemm: scheduler buffer allocation failed");
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep, sched);
+  const SkParams sk = sk_plan(tiles, grid / CG, (K + GEMM_BK - 1) / GEMM_BK, GEMM_BM * CG, BN, stream);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep, sk, sched);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return check_launch("gemm_tcgen05");
 }
@@ -510,7 +747,7 @@ static int preload_one() {
 }
 
 int gemm_preload() {
-  int rc = 0;
+  int rc = sk_alloc();
   rc |= preload_one<256, false, false, 1>(); rc |= preload_one<256, false, true, 1>();
   rc |= preload_one<256, true, false, 1>();  rc |= preload_one<256, true, true, 1>();
   rc |= preload_one<128, false, false, 1>(); rc |= preload_one<128, false, true, 1>();
@@ -540,6 +777,23 @@ static int dispatch(const void* A, long long lda, const void* B, long long ldb, 
 }  // namespace zpp
 
 static int g_cg_pref = 0;  // 0 = auto, 1 = force single-CTA tiles, 2 = prefer pairs
+
+// Debug: copy the last traced launch's timeline ([cta][32 items][item, mma0, mma1, epi0,
+// epi_acc, epi1] globaltimer ns) to host memory; returns the number of u64 copied.
+extern "C" long long zpp_gemm_trace_dump(unsigned long long* host, long long max_u64) {
+  if (!zpp::g_gemm_trace) return 0;
+  long long n = 148LL * zpp::GEMM_TRACE_ITEMS * 6;
+  if (n > max_u64) n = max_u64;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, zpp::g_gemm_trace, n * 8, cudaMemcpyDeviceToHost);
+  cudaMemset(zpp::g_gemm_trace, 0, 148ull * zpp::GEMM_TRACE_ITEMS * 6 * 8);
+  return n;
+}
+
+extern "C" int zpp_gemm_set_streamk(int on) {
+  zpp::g_sk_mode = on ? 1 : 0;
+  return ZPP_OK;
+}
 
 extern "C" int zpp_gemm_set_cta_group(int cg) {
   if (cg < 0 || cg > 2) return zpp::set_error(ZPP_ERR_ARG, "cta group must be 0, 1 or 2");

@@ -25,6 +25,7 @@ _SIGS = {
     "zpp_gemm": (c_int, [P, c_int, c_size, P, c_int, c_size, P, c_size, c_int, c_int, c_int, c_int,
                          P, P, c_size, P, c_size, c_stream]),
     "zpp_gemm_set_cta_group": (c_int, [c_int]),
+    "zpp_gemm_set_streamk": (c_int, [c_int]),
     "zpp_attn_set_impl": (c_int, [c_int]),
     "zpp_attn_fwd": (c_int, [P, P, P, c_int, c_int, c_int, c_int, c_stream]),
     "zpp_attn_bwd": (c_int, [P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_stream]),

@@ -91,6 +91,16 @@ def set_cta_group(cg: int) -> None:
     lib.call("zpp_gemm_set_cta_group", cg)
 
 
+def set_streamk(on: bool) -> None:
+    """Enable / disable the stream-K split of the GEMM's last partial wave."""
+    lib.call("zpp_gemm_set_streamk", int(on))
+
+
+def preload() -> None:
+    """Load every kernel and allocate the GEMM stream-K workspaces (idempotent)."""
+    lib.call("zpp_preload_kernels")
+
+
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
     _count(1)

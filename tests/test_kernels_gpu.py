@@ -32,6 +32,11 @@ def _seed():
     torch.manual_seed(0)
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _preload():
+    ops.preload()  # kernels + stream-K workspaces, as the engine does
+
+
 GEMM_SHAPES = [(128, 128, 64), (256, 512, 256), (200, 136, 72), (384, 1024, 320), (2048, 3072, 1024),
                (128, 50304, 256), (1000, 264, 4096)]
 
@@ -88,6 +93,44 @@ def test_gemm_gelu_and_dgelu(cta_group):
     gy = A.float() @ B.float().t()
     torch.nn.functional.gelu(u, approximate="tanh").backward(gy)
     assert rel_err(D, u.grad) < 1e-2
+
+
+# Shapes whose last wave is split into stream-K pieces at 148 SMs (74 pairs):
+# 2048x4096 -> 128 pair tiles (74 whole + 54 x 4 pieces); 2048x12288 -> 384 (370 + 14 x p).
+SK_SHAPES = [(2048, 4096, 4096), (2048, 12288, 1024), (2048, 4096, 16384), (1000, 4000, 2048)]
+
+
+@pytest.mark.parametrize("shape", SK_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_gemm_streamk(shape, cta_group):
+    M, N, K = shape
+    A, B, bias, resid = bf(M, K), bf(N, K, scale=0.05), bf(N), bf(M, N)
+    outs = []
+    for sk in (True, False, True):
+        ops.set_streamk(sk)
+        C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        ops.gemm(A, B, C, bias=bias, resid=resid)
+        F = torch.empty(M, N, device=dev, dtype=torch.float32)
+        ops.gemm(A, B, F, epilogue=ops.EPI_F32)
+        outs.append((C, F))
+    ops.set_streamk(True)
+    ref = A.float() @ B.float().t()
+    for C, F in outs:
+        assert rel_err(C, ref + bias.float() + resid.float()) < 1e-2
+        assert rel_err(F, ref) < 1e-5 * math.sqrt(K) + 1e-5
+    # deterministic: the split sums pieces in a fixed order
+    assert torch.equal(outs[0][0], outs[2][0]) and torch.equal(outs[0][1], outs[2][1])
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 2048), (12288, 4096, 2048)])
+def test_gemm_streamk_wgrad(M, N, K, cta_group):
+    A, B = bf(K, M), bf(K, N)
+    C = torch.randn(M, N, device=dev)
+    ref = C.clone() + A.float().t() @ B.float()
+    ops.gemm(A, B, C, a_t=True, b_t=True, epilogue=ops.EPI_F32_ACC)
+    assert rel_err(C, ref) < 1e-5
+    G = torch.empty(M, N, device=dev)
+    ops.gemm(A, B, G, a_t=True, b_t=True, epilogue=ops.EPI_F32)
+    assert rel_err(G, A.float().t() @ B.float()) < 1e-5
 
 
 @pytest.mark.parametrize("M,N,K", [(384, 256, 512), (1000, 264, 136)])

@@ -1,0 +1,42 @@
+"""Timeline of one GEMM launch (ZPP_GEMM_TRACE=1).  usage: gemm_trace.py M N K a_t b_t"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+os.environ["ZPP_GEMM_TRACE"] = "1"
+sys.path.insert(0, '.')
+from paper_2402_03791_b200.engine import lib, ops  # noqa: E402
+
+M, N, K = (int(x) for x in sys.argv[1:4])
+at, bt = sys.argv[4] == '1', sys.argv[5] == '1'
+ops.preload()
+bf = lambda *s: (torch.randn(*s, device='cuda') * 0.05).to(torch.bfloat16)  # noqa: E731
+A = bf(K, M) if at else bf(M, K)
+B = bf(K, N) if bt else bf(N, K)
+C = torch.zeros(M, N, device='cuda', dtype=torch.bfloat16)
+L = lib.load()
+L.zpp_gemm_trace_dump.restype = ctypes.c_longlong
+buf = np.zeros(148 * 32 * 6, dtype=np.uint64)
+for _ in range(3):
+    ops.gemm(A, B, C, a_t=at, b_t=bt)
+    torch.cuda.synchronize()
+    L.zpp_gemm_trace_dump(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_longlong(buf.size))
+t = buf.reshape(148, 32, 6).astype(np.int64)
+flag = (t[:, :, 5] >> 63) & 1
+t[:, :, 5] &= (1 << 62) - 1
+valid = t[:, :, 1] > 0
+t0 = t[:, :, 1][valid].min()
+print("cta it item  mma0  mma1 | epi0 epiacc epi1 (us from launch)")
+for c in list(range(0, 148, 2))[:int(os.environ.get("ROWS", "12"))]:
+    line = []
+    for i in range(32):
+        if t[c, i, 1] == 0:
+            break
+        r = t[c, i]
+        line.append(f"[{r[0]}: m {(r[1]-t0)/1e3:.1f}-{(r[2]-t0)/1e3:.1f} e {(r[3]-t0)/1e3:.1f}/{(r[4]-t0)/1e3:.1f}-{(r[5]-t0)/1e3:.1f}{'p' if flag[c,i] else ''}]")
+    print(c, " ".join(line))
+end = (t[:, :, 5][t[:, :, 5] > 0] - t0).max() / 1e3
+print("last epilogue end (us):", end)
