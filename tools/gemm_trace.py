@@ -1,4 +1,4 @@
-"""Timeline of one GEMM launch (ZPP_GEMM_TRACE=1).  usage: gemm_trace.py M N K a_t b_t"""
+"""Timeline of one GEMM launch (ZPP_GEMM_TRACE=1).  usage: gemm_trace.py M N K a_t b_t [bf16|f32|f32acc]"""
 import ctypes
 import os
 import sys
@@ -16,12 +16,14 @@ ops.preload()
 bf = lambda *s: (torch.randn(*s, device='cuda') * 0.05).to(torch.bfloat16)  # noqa: E731
 A = bf(K, M) if at else bf(M, K)
 B = bf(K, N) if bt else bf(N, K)
-C = torch.zeros(M, N, device='cuda', dtype=torch.bfloat16)
+epi = sys.argv[6] if len(sys.argv) > 6 else "bf16"
+C = torch.zeros(M, N, device='cuda', dtype=torch.bfloat16 if epi == "bf16" else torch.float32)
+EPI = {"bf16": ops.EPI_BF16, "f32": ops.EPI_F32, "f32acc": ops.EPI_F32_ACC}[epi]
 L = lib.load()
 L.zpp_gemm_trace_dump.restype = ctypes.c_longlong
 buf = np.zeros(148 * 32 * 6, dtype=np.uint64)
 for _ in range(3):
-    ops.gemm(A, B, C, a_t=at, b_t=bt)
+    ops.gemm(A, B, C, a_t=at, b_t=bt, epilogue=EPI)
     torch.cuda.synchronize()
     L.zpp_gemm_trace_dump(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_longlong(buf.size))
 t = buf.reshape(148, 32, 6).astype(np.int64)
