@@ -30,6 +30,16 @@ from .tasks import (
     schedule_to_json,
 )
 from .validation import FuzzSummary, Violation, ViolationKind, fuzz_check, validate
+from .simulation import (
+    MemoryBreakdown,
+    SimResult,
+    SimulationDeadlock,
+    bubble_count,
+    comm_volume,
+    peak_memory,
+    simulate,
+)
+from .render import RenderFormat, chrome_trace, render_timeline
 
 __version__ = "0.1.0"
 
@@ -40,6 +50,8 @@ __all__ = [
     "build_dependency_edges", "execute", "expected_edges", "export_text", "fuzz_check",
     "generate", "load_config", "make_placement", "schedule_from_json",
     "schedule_to_json", "validate", "__version__",
+    "MemoryBreakdown", "SimResult", "SimulationDeadlock", "bubble_count", "comm_volume",
+    "peak_memory", "simulate", "RenderFormat", "chrome_trace", "render_timeline",
 ]
 
 

@@ -51,6 +51,18 @@ class StepResult:
     exposed_comm_ms: float | None = None    # compute-stream waits on AG / RS
     p2p_wait_ms: float | None = None        # compute-stream waits on P2P recv (bubble + transfer)
     busy_ms: float | None = None
+    sim: object = None                      # timeline runtimes: the whole-job SimResult (engine.timeline)
+
+    def __getattr__(self, name):
+        # SimResult superset: makespan, per_device_busy/idle, bubble_ratios, peak_mem,
+        # comm_bytes_intra/inter, ... and the extras (loss, tokens_per_s, mfu, ...)
+        sim = self.__dict__.get("sim")
+        if sim is not None:
+            if hasattr(sim, name):
+                return getattr(sim, name)
+            if name in sim.extras:
+                return sim.extras[name]
+        raise AttributeError(name)
 
 
 class _Stage:
@@ -216,8 +228,14 @@ class Runtime:
             self.s_comp.wait_event(ev)
             e1 = self._record(self.s_comp, True)
             self._waits.append((kind, e0, e1))
+            self._task_start = e1  # the task's own work starts after its last wait
         else:
             self.s_comp.wait_event(ev)
+
+    def _begin(self, stream) -> None:
+        """Mark where a side-stream task's own work starts (after its stream waits)."""
+        if self.timeline:
+            self._task_start = self._record(stream, True)
 
     def _dev_of(self, s: int) -> int:
         return self.pl.stage_to_device[s]
@@ -254,9 +272,10 @@ class Runtime:
                           f"reserved={torch.cuda.memory_reserved(self.dev) / 1e9:.1f}G", flush=True)
                 stream = self._stream_of(task)
                 e0 = self._record(stream, True) if self.timeline else None
+                self._task_start = None
                 self._run(task)
                 if self.timeline:
-                    times[task] = (e0, self._record(stream, True))
+                    times[task] = (self._task_start or e0, self._record(stream, True))
         t_end = self._record(comp, True)
         torch.cuda.current_stream(self.dev).wait_stream(comp)
         self._t = (t_start, t_end, times)
@@ -311,6 +330,7 @@ class Runtime:
             st.ag_event = None
             return
         self.s_ag.wait_event(self.opt_event)  # shards are final once the previous OPT ran
+        self._begin(self.s_ag)
         ns = st.lay.shard_numel
         lib.call("zpp_allgather", self.comms[("ag", self.p)], st.shard_bf16.data_ptr(),
                  st.gathered.data_ptr(), ns, 0, self.s_ag.cuda_stream)
@@ -322,6 +342,7 @@ class Runtime:
             return  # the stage grad IS the shard grad; nothing moves (0 bytes)
         rs = self.s_rs
         rs.wait_event(self._record(self.s_comp))   # all B/W of (s, u) enqueued before this point
+        self._begin(rs)
         n, ns = st.lay.numel, st.lay.shard_numel
         send, recv = self.rs_send[:n], self.rs_recv[:ns]
         ops.cast_scale(st.grad_full, send, 1.0, stream=rs)
@@ -536,11 +557,20 @@ class Runtime:
 def execute(sched: Schedule, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
             runtime: Runtime, ids: torch.Tensor, labels: torch.Tensor) -> StepResult:
     """Run one ZeroPP training step of ``sched`` on this rank (the engine's
-    ``simulate``, `simulation.py:90`).  Returns a timed :class:`StepResult`."""
+    ``simulate``, `simulation.py:90`).  Returns a timed :class:`StepResult`; with a
+    ``timeline=True`` runtime it also carries the whole-job measured
+    :class:`~paper_2402_03791_b200.simulation.SimResult` (``res.sim``, fields readable
+    directly: ``res.makespan``, ``res.bubble_ratios``, ``res.loss`` ...) -- a
+    collective over all ranks when the job is multi-rank."""
     if sched is not runtime.sched:
         raise ValueError("runtime was built for a different schedule")
     t0 = time.perf_counter()
     res = runtime.step(ids, labels)
     res = runtime.finish_timing(res)
     res.host_s = time.perf_counter() - t0
+    if runtime.timeline:
+        from .timeline import measured_result
+        import torch.distributed as dist
+        gather = runtime.world > 1 and dist.is_available() and dist.is_initialized()
+        res.sim = measured_result(runtime, res, gather=gather)
     return res

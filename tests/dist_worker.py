@@ -34,6 +34,11 @@ def main():
         loss = loss_sum.item() / (D * B * spec.tokens_per_microbatch)
         loss_o, grads_o, new_o = oracle_for(spec, cfg, pl, tokens[0])
         fails = compare_shards(spec, cfg, pl, rt, grads_o, new_o)
+        sim = res[0].sim  # whole-job measured timeline gathered from every pipeline rank
+        if sim is None or set(sim.task_times) != set(sched.tasks()) or sim.extras.get("partial"):
+            fails.append("measured timeline does not cover every device's tasks")
+        elif not all(0 < b <= sim.makespan for b in sim.per_device_busy):
+            fails.append(f"measured busy/makespan inconsistent: {sim.per_device_busy} / {sim.makespan}")
         if abs(loss - loss_o) / loss_o > LOSS_RTOL:
             fails.append(f"loss {loss} vs oracle {loss_o}")
         if fails:

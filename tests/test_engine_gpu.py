@@ -44,6 +44,26 @@ def test_recompute_step_matches_oracle(B, U, V):
     assert not compare_shards(spec, cfg, pl, rt, grads_o, new_o)
 
 
+def test_measured_timeline_is_a_sim_result():
+    """execute() with a timeline runtime returns the SimResult superset."""
+    from paper_2402_03791_b200 import render_timeline
+    from paper_2402_03791_b200.engine.timeline import calibrate, predict
+    spec = GPTSpec.tiny()
+    rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, 1, 1, 8, 4, 2, steps=2)
+    r = res[1]
+    assert set(r.task_times) == set(sched.tasks())
+    assert 0 < r.per_device_busy[0] <= r.makespan <= r.step_ms * 1.001
+    assert r.per_device_idle[0] == r.makespan - r.per_device_busy[0]
+    assert r.bubble_ratios[0] >= 0 and r.tokens_per_s > 0 and 0 < r.mfu < 1
+    assert r.peak_mem_measured[0] > 0 and r.peak_mem[0] > 0
+    assert abs(r.loss - r.loss_sum.item() / (8 * spec.tokens_per_microbatch)) < 1e-6
+    txt = render_timeline(r.sim, sched)
+    assert txt.startswith("makespan=") and "d0" in txt
+    fitted, costs = calibrate(r.sim, sched, model, pl)
+    pred = predict(sched, fitted, costs, cfg, pl)
+    assert pred.makespan > 0
+
+
 def test_loss_decreases_over_steps():
     spec = GPTSpec.tiny(lr=1e-3)
     B = 4
