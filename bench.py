@@ -123,7 +123,7 @@ class Clocks:
 def run_zpp(args) -> None:
     import torch
     import torch.distributed as dist
-    from oracle.gpt_oracle import make_tokens  # synthetic-token generator only (seeded CPU randint)
+    from paper_2402_03791_b200.engine.data import synthetic_tokens as make_tokens
     from paper_2402_03791_b200 import ModelSpec, ParallelConfig, generate, make_placement
     from paper_2402_03791_b200.engine import GPTSpec, Runtime, execute, ops
 

@@ -50,3 +50,10 @@ def test_summarize_equals_simulate_on_same_times():
 def test_model_flops_gpt_6p2b():
     from paper_2402_03791_b200.engine import GPTSpec
     assert model_flops_per_token(GPTSpec.gpt_6p2b()) / 1e9 == pytest.approx(43.11, abs=0.01)
+
+
+def test_engine_tokens_equal_oracle_tokens():
+    from oracle.gpt_oracle import make_tokens
+    from paper_2402_03791_b200.engine.data import synthetic_tokens
+    import torch
+    assert torch.equal(synthetic_tokens(2, 2, 3, 1, 16, 50304), make_tokens(2, 2, 3, 1, 16, 50304))
