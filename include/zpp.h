@@ -128,6 +128,8 @@ int zpp_comm_destroy(void* comm);
 int zpp_allgather(void* comm, const void* send, void* recv, long long count_per_rank, int dtype, uintptr_t stream);
 int zpp_reduce_scatter(void* comm, const void* send, void* recv, long long count_per_rank, int dtype,
                        uintptr_t stream);
+/* outer (inter-node) DP: AR_GRAD (schedules.py:80-81); sum over the comm's ranks */
+int zpp_allreduce(void* comm, const void* send, void* recv, long long count, int dtype, uintptr_t stream);
 int zpp_send(void* comm, const void* buf, long long count, int dtype, int peer, uintptr_t stream);
 int zpp_recv(void* comm, void* buf, long long count, int dtype, int peer, uintptr_t stream);
 

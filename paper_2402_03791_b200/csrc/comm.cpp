@@ -24,6 +24,7 @@ struct Nccl {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -54,6 +55,7 @@ extern "C" int zpp_nccl_load(const char* path) {
   SYM(CommDestroy, "ncclCommDestroy");
   SYM(AllGather, "ncclAllGather");
   SYM(ReduceScatter, "ncclReduceScatter");
+  SYM(AllReduce, "ncclAllReduce");
   SYM(Send, "ncclSend");
   SYM(Recv, "ncclRecv");
   SYM(GetErrorString, "ncclGetErrorString");
@@ -100,6 +102,14 @@ extern "C" int zpp_reduce_scatter(void* comm, const void* send, void* recv, long
   ncclResult_t r = g.ReduceScatter(send, recv, (size_t)count, dt(dtype), nccl_sum, comm,
                                    reinterpret_cast<cudaStream_t>(stream));
   return r ? nccl_err(r, "ncclReduceScatter") : ZPP_OK;
+}
+
+extern "C" int zpp_allreduce(void* comm, const void* send, void* recv, long long count, int dtype,
+                             uintptr_t stream) {
+  if (int rc = need()) return rc;
+  ncclResult_t r = g.AllReduce(send, recv, (size_t)count, dt(dtype), nccl_sum, comm,
+                               reinterpret_cast<cudaStream_t>(stream));
+  return r ? nccl_err(r, "ncclAllReduce") : ZPP_OK;
 }
 
 extern "C" int zpp_send(void* comm, const void* buf, long long count, int dtype, int peer, uintptr_t stream) {

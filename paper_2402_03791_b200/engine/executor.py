@@ -1,13 +1,16 @@
 """Per-rank ZeroPP step executor: the real-hardware replacement for the
 reference's ``simulate`` (`pkg/src/zeroppsim/simulation.py:90-158`).
 
-One OS process per GPU; rank r is pipeline rank p = r // D and ZeRO index
-z = r % D.  The host walks ``sched.per_device[p]`` in order and only enqueues
+One OS process per GPU; rank r = node*P*D + p*D + z: node is the outer
+data-parallel replica (``inter_node_dp`` = n "nodes"; one box emulates them), p the
+pipeline rank and z the ZeRO index.  The host walks ``sched.per_device[p]`` in order and only enqueues
 work; ordering across streams uses CUDA events:
 
     compute    F / B / W (GPT stage math, libzpp kernels), OPT (sharded AdamW)
     ag         AG_PARAM: ncclAllGather of the stage's bf16 shard (in place)
     rs         RS_GRAD : fp32 stage grad -> bf16 wire -> ncclReduceScatter -> += fp32 shard grad
+               AR_GRAD / RS_GRAD_INTER: the shard grad across the n replicas (outer tail)
+    ag         AG_PARAM_INTER: bf16 optimizer sub-shards -> full shard (ZeRO-1 outer mode)
     act_send / act_recv / grad_send / grad_recv: stage-boundary P2P
 
 P2P uses one dedicated 2-rank communicator per (message kind, directed pair):
@@ -33,10 +36,44 @@ from ..config import HybridMode, ModelSpec, ParallelConfig, Placement, Recompute
 from ..tasks import Schedule, Task, TaskKind
 from ..validation import validate
 from . import lib, ops
-from .model import GPTSpec, StageLayout, init_offset, shard_init_ranges, stage_layout
+from .model import GPTSpec, StageLayout, init_offset, optimizer_sub, shard_init_ranges, stage_layout
 
 BF16, F32 = torch.bfloat16, torch.float32
 _TRACE = os.environ.get("ZPP_TRACE") == "1"
+
+
+def rank_coords(rank: int, n: int, P: int, D: int) -> tuple[int, int, int]:
+    """rank -> (node, pipeline rank p, ZeRO index z); rank = node*P*D + p*D + z."""
+    if not 0 <= rank < n * P * D:
+        raise ValueError(f"rank {rank} outside n*P*D = {n * P * D}")
+    node, local = divmod(rank, P * D)
+    return node, local // D, local % D
+
+
+def comm_plan(n: int, P: int, D: int) -> list[tuple[tuple, list[int]]]:
+    """Every NCCL communicator of an n x P x D job as (key, global ranks), in the one
+    global creation order all ranks follow.  Keys are node-local (each rank joins only
+    its own node's): ("ag", p) / ("rs", p) = ZeRO group p (one per stream);
+    ("act", p, p+1, z) / ("grad", p, p-1, z) = directed 2-rank P2P channels (ring wrap,
+    `config.py:186`); ("inter",) = the n replicas of one (p, z) shard (outer tail)."""
+    plan = []
+    for node in range(n):
+        base = node * P * D
+        for p in range(P):
+            grp = [base + p * D + z for z in range(D)]
+            if D > 1:
+                plan.append((("ag", p), grp))
+                plan.append((("rs", p), grp))
+        if P > 1:
+            for z in range(D):
+                for p in range(P):
+                    nxt, prv = (p + 1) % P, (p - 1) % P
+                    plan.append((("act", p, nxt, z), [base + p * D + z, base + nxt * D + z]))
+                    plan.append((("grad", p, prv, z), [base + p * D + z, base + prv * D + z]))
+    if n > 1:
+        for local in range(P * D):
+            plan.append((("inter",), [node * P * D + local for node in range(n)]))
+    return plan
 
 
 @dataclass
@@ -66,17 +103,24 @@ class StepResult:
 
 
 class _Stage:
-    """Buffers and views of one pipeline stage held by this rank."""
+    """Buffers and views of one pipeline stage held by this rank.
 
-    def __init__(self, lay: StageLayout, D: int, z: int, dev):
+    ZeRO-1 outer mode (``sub`` = n > 1): the rank keeps the whole bf16 shard but
+    Adam state only for optimizer sub-shard ``node`` of it (``ns / n`` elements)."""
+
+    def __init__(self, lay: StageLayout, D: int, z: int, dev, sub: int = 1, node: int = 0):
         self.lay = lay
         n, ns = lay.numel, lay.shard_numel
+        nsub = ns // sub
+        self.sub, self.nsub = sub, nsub
         self.gathered = torch.zeros(n, dtype=BF16, device=dev)
         self.shard_bf16 = self.gathered[z * ns:(z + 1) * ns]      # in-place all-gather layout
-        self.master = torch.zeros(ns, dtype=F32, device=dev)
-        self.exp_avg = torch.zeros(ns, dtype=F32, device=dev)
-        self.exp_avg_sq = torch.zeros(ns, dtype=F32, device=dev)
+        self.sub_bf16 = self.shard_bf16[node * nsub:(node + 1) * nsub]  # AG_PARAM_INTER layout
+        self.master = torch.zeros(nsub, dtype=F32, device=dev)
+        self.exp_avg = torch.zeros(nsub, dtype=F32, device=dev)
+        self.exp_avg_sq = torch.zeros(nsub, dtype=F32, device=dev)
         self.grad_shard = torch.zeros(ns, dtype=F32, device=dev)
+        self.grad_sub = self.grad_shard if sub == 1 else torch.zeros(nsub, dtype=F32, device=dev)
         self.grad_full = self.grad_shard if D == 1 else torch.zeros(n, dtype=F32, device=dev)
         self.p: dict = {}
         self.g: dict = {}
@@ -113,22 +157,23 @@ class Runtime:
     def __init__(self, spec: GPTSpec, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False):
-        if world != cfg.pp_size * cfg.dp_size:
-            raise ValueError(f"world size {world} != P*D = {cfg.pp_size * cfg.dp_size}")
+        if world != cfg.pp_size * cfg.dp_size * cfg.inter_node_dp:
+            raise ValueError(f"world size {world} != n*P*D = "
+                             f"{cfg.inter_node_dp * cfg.pp_size * cfg.dp_size}")
         if model.num_layers != spec.num_layers or model.hidden_size != spec.hidden or \
                 model.seq_len != spec.seq_len:
             raise ValueError("ModelSpec and GPTSpec disagree on L / h / s")
         if cfg.microbatch_samples != spec.microbatch_samples:
             raise ValueError("ParallelConfig.microbatch_samples != GPTSpec.microbatch_samples")
-        if cfg.inter_node_dp > 1:
-            raise NotImplementedError("inter_node_dp > 1 (outer DP / ZeRO-1) is a 'next' row")
         bad = validate(sched, placement, cfg)
         if bad:
             raise ValueError(f"schedule failed validation: {bad[0]}")
         self.spec, self.model, self.cfg, self.pl, self.sched = spec, model, cfg, placement, sched
         self.rank, self.world = rank, world
-        self.P, self.D = cfg.pp_size, cfg.dp_size
-        self.p, self.z = rank // self.D, rank % self.D
+        self.P, self.D, self.n = cfg.pp_size, cfg.dp_size, cfg.inter_node_dp
+        self.node, self.p, self.z = rank_coords(rank, self.n, self.P, self.D)
+        self.dp_index = self.node * self.D + self.z     # which slice of the global batch
+        self.sub = optimizer_sub(cfg)
         self.S = cfg.num_stages
         self.timeline = timeline
         if device is None:
@@ -141,8 +186,8 @@ class Runtime:
         self.local_stages = placement.device_stages(self.p)
         self.stages: dict[int, _Stage] = {}
         for s in self.local_stages:
-            lay = stage_layout(spec, s, self.S, placement.stage_to_layers[s], self.D)
-            self.stages[s] = _Stage(lay, self.D, self.z, self.dev)
+            lay = stage_layout(spec, s, self.S, placement.stage_to_layers[s], self.D, self.sub)
+            self.stages[s] = _Stage(lay, self.D, self.z, self.dev, self.sub, self.node)
         mk = lambda: torch.cuda.Stream(device=self.dev)  # noqa: E731
         self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
         self.s_act_send, self.s_act_recv, self.s_grad_send, self.s_grad_recv = mk(), mk(), mk(), mk()
@@ -155,7 +200,7 @@ class Runtime:
                                    dtype=F32, device=self.dev)
         max_n = max(st.lay.numel for st in self.stages.values())
         max_ns = max(st.lay.shard_numel for st in self.stages.values())
-        if self.D > 1:
+        if self.D > 1 or self.n > 1:
             self.rs_send = torch.empty(max_n, dtype=BF16, device=self.dev)
             self.rs_recv = torch.empty(max_ns, dtype=BF16, device=self.dev)
         self.loss_sum = torch.zeros(1, dtype=F32, device=self.dev)
@@ -168,22 +213,12 @@ class Runtime:
 
     # ------------------------------------------------------------------ setup
     def _init_comms(self) -> None:
-        """Create ZeRO and P2P communicators in one global order (no init deadlock)."""
+        """Create ZeRO, P2P and outer communicators in one global order (no init deadlock).
+        Keys are node-local; a rank only joins the communicators of its own node, plus
+        ("inter",) = its (p, z) peers in the other n - 1 replicas."""
         import torch.distributed as dist
         lib.load_nccl()
-        P, D = self.P, self.D
-        plan = []  # (key, ranks)
-        for p in range(P):
-            grp = [p * D + z for z in range(D)]
-            if D > 1:
-                plan.append((("ag", p), grp))
-                plan.append((("rs", p), grp))
-        if P > 1:
-            for z in range(D):
-                for p in range(P):
-                    nxt, prv = (p + 1) % P, (p - 1) % P
-                    plan.append((("act", p, nxt, z), [p * D + z, nxt * D + z]))
-                    plan.append((("grad", p, prv, z), [p * D + z, prv * D + z]))
+        plan = comm_plan(self.n, self.P, self.D)
         import ctypes
         uids = []
         if self.rank == 0:
@@ -201,12 +236,16 @@ class Runtime:
                 self.comms[key] = handle
 
     def init_params(self) -> None:
-        """Deterministic init of this rank's shards (identical for every P x D split)."""
+        """Deterministic init of this rank's shards (identical for every n x P x D split)."""
         with torch.cuda.stream(self.s_comp):
             for st in self.stages.values():
+                full = st.master if st.sub == 1 else torch.empty(st.lay.shard_numel, dtype=F32, device=self.dev)
                 for slot, t0, s0, cnt in shard_init_ranges(st.lay, self.z):
-                    ops.init_param(st.master[s0:s0 + cnt], st.shard_bf16[s0:s0 + cnt], self.spec.seed,
+                    ops.init_param(full[s0:s0 + cnt], st.shard_bf16[s0:s0 + cnt], self.spec.seed,
                                    init_offset(slot.uid) + t0, slot.mean, slot.std, stream=self.s_comp)
+                if st.sub > 1:
+                    st.master.copy_(full[self.node * st.nsub:(self.node + 1) * st.nsub])
+                    full.record_stream(self.s_comp)
         self.opt_event = self._record(self.s_comp)
         if self.D == 1:
             for st in self.stages.values():
@@ -256,7 +295,7 @@ class Runtime:
         self._local_grad: dict = {}
         self._waits: list = []
         self._rs_events: list = []
-        self._grad_scale = 1.0 / (self.D * B * b * s_len)
+        self._grad_scale = 1.0 / (self.n * self.D * B * b * s_len)
         self.step_count += 1
         times = {}
         comp = self.s_comp
@@ -295,9 +334,9 @@ class Runtime:
         return res
 
     def _stream_of(self, task: Task):
-        if task.kind is TaskKind.AG_PARAM:
+        if task.kind in (TaskKind.AG_PARAM, TaskKind.AG_PARAM_INTER):
             return self.s_ag
-        if task.kind is TaskKind.RS_GRAD:
+        if task.kind in (TaskKind.RS_GRAD, TaskKind.AR_GRAD, TaskKind.RS_GRAD_INTER):
             return self.s_rs
         return self.s_comp
 
@@ -317,9 +356,12 @@ class Runtime:
             self._reduce_scatter(task.stage)
         elif k is TaskKind.OPT:
             self._optimizer()
-        elif k in (TaskKind.RS_GRAD_INTER, TaskKind.AG_PARAM_INTER, TaskKind.AR_GRAD):
-            if task.bytes:
-                raise NotImplementedError("outer (inter-node) collectives are a 'next' row")
+        elif k is TaskKind.AR_GRAD:
+            self._outer_grad(reduce_scatter=False)
+        elif k is TaskKind.RS_GRAD_INTER:
+            self._outer_grad(reduce_scatter=True)
+        elif k is TaskKind.AG_PARAM_INTER:
+            self._outer_gather()
         else:
             raise NotImplementedError(f"task kind {k}")
 
@@ -327,8 +369,7 @@ class Runtime:
     def _all_gather(self, s: int) -> None:
         st = self.stages[s]
         if self.D == 1:
-            st.ag_event = None
-            return
+            return  # nothing moves; the previous AG_PARAM_INTER's event (if any) stays armed
         self.s_ag.wait_event(self.opt_event)  # shards are final once the previous OPT ran
         self._begin(self.s_ag)
         ns = st.lay.shard_numel
@@ -354,16 +395,61 @@ class Runtime:
         ops.accum(recv, st.grad_shard, stream=rs)
         self._rs_events.append(self._record(rs))
 
+    def _outer_grad(self, reduce_scatter: bool) -> None:
+        """AR_GRAD (DP outer, `schedules.py:80-81`) or RS_GRAD_INTER (ZeRO-1 outer,
+        `:83-84`): the fp32 shard grads of every local stage summed over the n replicas
+        holding the same (p, z) shard, on a bf16 wire (the bytes the reference models).
+        AR leaves the sum in ``grad_shard``; RS leaves sub-shard ``node`` in ``grad_sub``."""
+        if self.n == 1:
+            return  # 0-byte task (ZeRO-1 mode on one node)
+        rs = self.s_rs
+        rs.wait_event(self._record(self.s_comp))  # D == 1: W wrote grad_shard on compute
+        self._begin(rs)
+        comm = self.comms[("inter",)]
+        for st in self.stages.values():
+            ns, nsub = st.lay.shard_numel, st.nsub
+            wire = self.rs_send[:ns]
+            ops.cast_scale(st.grad_shard, wire, 1.0, stream=rs)
+            if reduce_scatter:
+                recv = self.rs_recv[:nsub]
+                lib.call("zpp_reduce_scatter", comm, wire.data_ptr(), recv.data_ptr(), nsub, 0, rs.cuda_stream)
+                ops.accum(recv, st.grad_sub, stream=rs)   # grad_sub is zero between steps
+            else:
+                lib.call("zpp_allreduce", comm, wire.data_ptr(), wire.data_ptr(), ns, 0, rs.cuda_stream)
+                ops.zero(st.grad_shard, stream=rs)
+                ops.accum(wire, st.grad_shard, stream=rs)
+        self._rs_events.append(self._record(rs))
+
+    def _outer_gather(self) -> None:
+        """AG_PARAM_INTER (`schedules.py:86-87`): every replica's updated bf16 sub-shard
+        -> the full bf16 shard (in place); the next use of the params waits for it."""
+        if self.n == 1:
+            return
+        ag = self.s_ag
+        ag.wait_event(self.opt_event)
+        self._begin(ag)
+        comm = self.comms[("inter",)]
+        for st in self.stages.values():
+            lib.call("zpp_allgather", comm, st.sub_bf16.data_ptr(), st.shard_bf16.data_ptr(), st.nsub, 0,
+                     ag.cuda_stream)
+        ev = self._record(ag)
+        self.opt_event = ev            # AG_PARAM of the next step gathers the updated shard
+        if self.D == 1:
+            for st in self.stages.values():
+                st.ag_event = ev       # no AG_PARAM event to wait on: first use waits here
+
     def _optimizer(self) -> None:
         for ev in self._rs_events:
             self._wait(ev, "zero")
         spec = self.spec
         for st in self.stages.values():
-            ops.adamw(st.master, st.exp_avg, st.exp_avg_sq, st.grad_shard, st.shard_bf16, spec.lr, spec.beta1,
+            ops.adamw(st.master, st.exp_avg, st.exp_avg_sq, st.grad_sub, st.sub_bf16, spec.lr, spec.beta1,
                       spec.beta2, spec.adam_eps, spec.weight_decay, self.step_count, stream=self.s_comp)
         if self.capture_grads:
-            self.captured = {s: st.grad_shard.clone() for s, st in self.stages.items()}
+            self.captured = {s: st.grad_sub.clone() for s, st in self.stages.items()}
         for st in self.stages.values():
+            if st.sub > 1:
+                ops.zero(st.grad_sub, stream=self.s_comp)    # inter reduce-scatter accumulates here
             if self.D > 1:
                 ops.zero(st.grad_shard, stream=self.s_comp)  # reduce-scatter results accumulate here
             else:

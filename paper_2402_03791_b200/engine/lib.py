@@ -51,6 +51,7 @@ _SIGS = {
     "zpp_comm_destroy": (c_int, [P]),
     "zpp_allgather": (c_int, [P, P, P, c_size, c_int, c_stream]),
     "zpp_reduce_scatter": (c_int, [P, P, P, c_size, c_int, c_stream]),
+    "zpp_allreduce": (c_int, [P, P, P, c_size, c_int, c_stream]),
     "zpp_send": (c_int, [P, P, c_size, c_int, c_int, c_stream]),
     "zpp_recv": (c_int, [P, P, c_size, c_int, c_int, c_stream]),
 }

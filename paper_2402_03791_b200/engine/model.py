@@ -12,8 +12,9 @@ Layout of stage s with layers [lo, hi) (each tensor 64-element aligned):
     per layer: ln1_g, ln1_b, w_qkv [3h, h], b_qkv, w_proj [h, h], b_proj,
                ln2_g, ln2_b, w_fc1 [4h, h], b_fc1, w_fc2 [h, 4h], b_fc2
     s == S-1 : lnf_g, lnf_b, w_lm [V, h]
-The flat size is padded to a multiple of 64*D so every ZeRO shard is 128-byte
-aligned.  Shard z of D owns elements [z*n/D, (z+1)*n/D).
+The flat size is padded to a multiple of 64*D (64*D*n in ZeRO-1 outer mode) so every
+ZeRO shard (and optimizer sub-shard) is 128-byte aligned.  Shard z of D owns elements
+[z*n/D, (z+1)*n/D).
 """
 
 from __future__ import annotations
@@ -125,7 +126,9 @@ class StageLayout:
 
 
 def stage_layout(spec: GPTSpec, stage: int, num_stages: int, layer_range: tuple[int, int],
-                 dp: int) -> StageLayout:
+                 dp: int, sub: int = 1) -> StageLayout:
+    """``sub`` > 1 (ZeRO-1 outer mode, n nodes) additionally makes every shard split
+    into ``sub`` equal, 128-byte aligned optimizer sub-shards."""
     h, V, L = spec.hidden, spec.vocab, spec.num_layers
     std, proj_std = spec.init_std, spec.init_std / math.sqrt(2.0 * L)
     lay = StageLayout(stage, layer_range)
@@ -156,9 +159,16 @@ def stage_layout(spec: GPTSpec, stage: int, num_stages: int, layer_range: tuple[
         add("lnf_g", None, (h,), 3, mean=1.0)
         add("lnf_b", None, (h,), 4)
         add("w_lm", None, (V, h), 5, sd=std)
-    lay.numel = _align(off, ALIGN * dp)
+    lay.numel = _align(off, ALIGN * dp * sub)
     lay.shard_numel = lay.numel // dp
     return lay
+
+
+def optimizer_sub(cfg) -> int:
+    """Optimizer sub-shards per ZeRO shard: n in ZeRO-1 outer mode (RS_GRAD_INTER /
+    AG_PARAM_INTER, `schedules.py:425-427`), else 1 (DP outer mode replicates Adam)."""
+    from ..config import HybridMode
+    return cfg.inter_node_dp if cfg.hybrid_mode is HybridMode.ZERO1_OUTER else 1
 
 
 def init_offset(uid: int) -> int:

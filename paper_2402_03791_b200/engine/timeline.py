@@ -47,7 +47,7 @@ def measured_result(runtime, res, gather: bool = True, peak_flops: float = 2.25e
     rt = runtime
     mine = [(t.task_id, s, e) for t, (s, e) in res.task_times.items()]
     peak_alloc = float(torch.cuda.max_memory_allocated(rt.dev))
-    local = {"p": rt.p, "z": rt.z, "times": mine, "peak": peak_alloc, "step_ms": res.step_ms,
+    local = {"p": rt.p, "z": rt.z, "node": rt.node, "times": mine, "peak": peak_alloc, "step_ms": res.step_ms,
              "loss_sum": float(res.loss_sum.item()), "tokens": res.tokens,
              "exposed": res.exposed_comm_ms or 0.0, "p2p": res.p2p_wait_ms or 0.0}
     if gather and rt.world > 1:
@@ -62,12 +62,12 @@ def measured_result(runtime, res, gather: bool = True, peak_flops: float = 2.25e
     peaks = [0.0] * sched.num_devices
     for part in parts:
         peaks[part["p"]] = max(peaks[part["p"]], part["peak"])
-        if part["z"] != 0:
+        if part["z"] != 0 or part["node"] != 0:
             continue
         for tid, s, e in part["times"]:
             times[by_id[tid]] = (s, e)
     cfg, spec = rt.cfg, rt.spec
-    tokens_job = cfg.dp_size * cfg.microbatches * spec.tokens_per_microbatch
+    tokens_job = cfg.inter_node_dp * cfg.dp_size * cfg.microbatches * spec.tokens_per_microbatch
     step_ms = max(p["step_ms"] for p in parts)
     loss_sum = sum(p["loss_sum"] for p in parts)
     tok_s = tokens_job / (step_ms / 1e3)
@@ -91,9 +91,10 @@ def measured_result(runtime, res, gather: bool = True, peak_flops: float = 2.25e
 
 def calibrate(measured: SimResult, sched: Schedule, model: ModelSpec, placement) -> tuple[ModelSpec, CommCostModel]:
     """Per-layer F/B/W/OPT costs (median ms per layer) and an effective intra-node
-    bandwidth (bytes/ms) fitted to a measured step."""
+    bandwidth (bytes/ms) fitted to a measured step; the inter-node bandwidth is fitted
+    to the outer tasks (AR_GRAD / RS_GRAD_INTER / AG_PARAM_INTER) when they moved bytes."""
     per_layer = {k: [] for k in (TaskKind.F, TaskKind.B, TaskKind.W, TaskKind.R)}
-    opt, comm_bw = [], []
+    opt, comm_bw, inter_bw = [], [], []
     for t, (s, e) in measured.task_times.items():
         if t.kind in per_layer and t.stage is not None:
             per_layer[t.kind].append((e - s) / placement.layers_in_stage(t.stage))
@@ -101,14 +102,15 @@ def calibrate(measured: SimResult, sched: Schedule, model: ModelSpec, placement)
             opt.append((e - s) / max(1, sum(placement.layers_in_stage(st)
                                           for st in placement.device_stages(t.device))))
         elif t.is_comm and t.bytes > 0 and e > s:
-            comm_bw.append(t.bytes / (e - s))
+            inter = t.kind in (TaskKind.AR_GRAD, TaskKind.RS_GRAD_INTER, TaskKind.AG_PARAM_INTER)
+            (inter_bw if inter else comm_bw).append(t.bytes / (e - s))
     med = lambda xs, d: statistics.median(xs) if xs else d  # noqa: E731
     fitted = dataclasses.replace(model, t_forward=med(per_layer[TaskKind.F], model.t_forward),
                                  t_input_grad=med(per_layer[TaskKind.B], model.t_input_grad),
                                  t_weight_grad=med(per_layer[TaskKind.W], model.t_weight_grad),
                                  t_optstep=med(opt, model.t_optstep))
     bw = med(comm_bw, 1e30)
-    return fitted, CommCostModel(intra_node_bandwidth=bw, inter_node_bandwidth=bw)
+    return fitted, CommCostModel(intra_node_bandwidth=bw, inter_node_bandwidth=med(inter_bw, bw))
 
 
 def predict(sched: Schedule, fitted: ModelSpec, costs: CommCostModel, cfg, placement) -> SimResult:

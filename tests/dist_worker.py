@@ -1,6 +1,8 @@
 """One rank of a multi-GPU ZeroPP step under torchrun; compares its shards with the oracle.
 
-usage: torchrun --nproc-per-node P*D dist_worker.py P D B U V OUTDIR
+usage: torchrun --nproc-per-node n*P*D dist_worker.py P D B U V OUTDIR [n MODE]
+
+n = inter_node_dp replicas emulated on one box, MODE = dp_outer | zero1_outer.
 """
 
 import os
@@ -16,22 +18,27 @@ sys.path.insert(0, HERE)
 sys.path.insert(0, os.path.dirname(HERE))
 
 from engine_harness import LOSS_RTOL, compare_shards, oracle_for, run_engine_step  # noqa: E402
+from paper_2402_03791_b200 import HybridMode  # noqa: E402
 from paper_2402_03791_b200.engine import GPTSpec  # noqa: E402
 
 
 def main():
     P, D, B, U, V = (int(x) for x in sys.argv[1:6])
     out = sys.argv[6]
+    n = int(sys.argv[7]) if len(sys.argv) > 7 else 1
+    mode = sys.argv[8] if len(sys.argv) > 8 else "dp_outer"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("gloo")
     spec = GPTSpec.tiny()
     msg = "OK"
     try:
-        rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, P, D, B, U, V, rank=rank, world=world)
+        rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, P, D, B, U, V, rank=rank, world=world,
+                                                                    inter_node_dp=n,
+                                                                    hybrid_mode=HybridMode(mode))
         loss_sum = torch.tensor([res[0].loss_sum.item()])
         dist.all_reduce(loss_sum)
-        loss = loss_sum.item() / (D * B * spec.tokens_per_microbatch)
+        loss = loss_sum.item() / (n * D * B * spec.tokens_per_microbatch)
         loss_o, grads_o, new_o = oracle_for(spec, cfg, pl, tokens[0])
         fails = compare_shards(spec, cfg, pl, rt, grads_o, new_o)
         sim = res[0].sim  # whole-job measured timeline gathered from every pipeline rank

@@ -91,3 +91,23 @@ def test_multi_gpu_step_matches_oracle(tmp_path, P, D, B, U, V):
     for rank in range(P * D):
         txt = (tmp_path / f"rank{rank}.txt").read_text()
         assert txt.startswith("OK"), txt
+
+
+@pytest.mark.parametrize("n,P,D,B,U,V,mode", [
+    (2, 1, 1, 4, 2, 2, "dp_outer"), (2, 1, 1, 4, 2, 2, "zero1_outer"),
+    (2, 2, 1, 8, 4, 2, "dp_outer"), (2, 1, 2, 4, 2, 1, "zero1_outer"), (2, 2, 1, 8, 4, 1, "zero1_outer")])
+def test_outer_dp_step_matches_oracle(tmp_path, n, P, D, B, U, V, mode):
+    """n emulated nodes x (P x D): AR_GRAD (DP outer) or RS_GRAD_INTER + AG_PARAM_INTER
+    (ZeRO-1 outer) over the replicas (schedules.py:80-87, 144-163, 425-429)."""
+    world = n * P * D
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs (run via gpurun --gpus {world})")
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(here, "dist_worker.py"),
+           str(P), str(D), str(B), str(U), str(V), str(tmp_path), str(n), mode]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for rank in range(world):
+        txt = (tmp_path / f"rank{rank}.txt").read_text()
+        assert txt.startswith("OK"), txt
