@@ -37,6 +37,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tokens/s/box GPT-6.2B ZeroPP at 1/2/4/8 B200; MFU; exposed comm ms/step"
 SPLITS = {1: (1, 1, 8, 2, 1), 2: (2, 1, 16, 8, 2), 4: (2, 2, 16, 8, 2), 8: (2, 4, 16, 8, 2)}
+# other BASELINE configs (parity cases; measured with --model / --split, not the headline line)
+MODELS = {"gpt-6.2b": ("gpt_6p2b", "GPT-6.2B (L32 h4096 a32 s2048 V50304, untied head)"),
+          "gpt-1.3b": ("gpt_1p3b", "GPT-1.3B (L24 h2048 a16 s2048 V50304, untied head)"),
+          "llama-7b": ("llama_7b", "LLaMA-7B (L32 h4096 a32 s4096 V32000, SwiGLU 11008, RoPE, RMSNorm)")}
 PEAK_DENSE_TF = 2250.0
 
 
@@ -47,6 +51,17 @@ def _peaks():
         return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
     except Exception:
         return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def _gemm_traffic():
+    """Per-launch DRAM bytes of the GEMM launches of one step, from the committed ncu
+    capture summary (tools/gemm_traffic.py -> profiles/gemm_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            d = json.load(f)
+        return d["dram_bytes_per_launch"], d["algorithmic_bytes_per_launch"]
+    except Exception:
+        return None, None
 
 
 # --------------------------------------------------------------------------- CPU leg
@@ -136,8 +151,8 @@ def run_zpp(args) -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo")
-    P, D, B, U, V = SPLITS[N]
-    spec = GPTSpec.gpt_6p2b()
+    P, D, B, U, V = _split(args)
+    spec = getattr(GPTSpec, MODELS[args.model][0])()
     model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
     cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V)
     pl = make_placement(cfg, model)
@@ -224,14 +239,16 @@ def run_zpp(args) -> None:
         value = tokens_per_step * args.steps / (dev_ms / 1e3)
         flops_tok = spec.flops_per_token()
         achieved_tf = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+        traffic, alg_bytes = _gemm_traffic()
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": N,
+            "metric": METRIC if args.model == "gpt-6.2b" else METRIC.replace("GPT-6.2B", args.model.upper()),
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded CPU randint tokens, deterministic counter-hash init)",
-            "config": {"workload": f"GPT-6.2B ZeroPP step, P{P} x D{D}, B={B} micro-batches/ZeRO rank, "
-                                   f"U={U}, V={V}, b=1, s=2048",
-                       "model": "GPT-6.2B (L32 h4096 a32 s2048 V50304, untied head)",
+            "config": {"workload": f"{args.model.upper()} ZeroPP step, P{P} x D{D}, B={B} micro-batches/ZeRO "
+                                   f"rank, U={U}, V={V}, b=1, s={spec.seq_len}",
+                       "model": MODELS[args.model][1],
                        "global_batch": D * B, "seq_len": spec.seq_len, "parallelism": f"pp{P}xzero{D}",
                        "tokens_per_step": tokens_per_step,
                        "l2": "inputs larger than L2 (each step streams >10 GB of weights/activations)"},
@@ -248,7 +265,10 @@ def run_zpp(args) -> None:
                          "achieved": round(achieved_tf, 1) if achieved_tf else None, "peak": sustained,
                          "peak_kind": f"{kind} sustained bf16", "unit": "TFLOP/s",
                          "frac": round(achieved_tf / sustained, 4) if achieved_tf else None,
-                         "gemm_launches": gemm_calls, "traffic": None},
+                         "gemm_launches": gemm_calls,
+                         "traffic": round(traffic) if traffic else None,
+                         "traffic_unit": "DRAM bytes per GEMM launch (ncu, profiles/gemm_traffic.json)",
+                         "algorithmic_bytes_per_launch": round(alg_bytes) if alg_bytes else None},
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -258,6 +278,16 @@ def run_zpp(args) -> None:
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _split(args):
+    if not args.split:
+        return SPLITS[args.gpus]
+    pd, B, U, V = args.split.split(":")
+    P, D = (int(x) for x in pd.lower().split("x"))
+    if P * D != args.gpus:
+        raise SystemExit(f"--split {args.split}: P*D != --gpus {args.gpus}")
+    return P, D, int(B), int(U), int(V)
 
 
 def run_reference(args) -> None:
@@ -295,6 +325,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="zpp", choices=["zpp", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--model", default="gpt-6.2b", choices=sorted(MODELS))
+    ap.add_argument("--split", default=None, help="PxD:B:U:V override of the default split for --gpus")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out"))
     args = ap.parse_args()
     os.makedirs(args.out_dir, exist_ok=True)

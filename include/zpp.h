@@ -87,6 +87,21 @@ int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const fl
                       int cols, int accumulate, uintptr_t stream);
 long long zpp_layernorm_bwd_workspace_floats(int rows, int cols);
 
+/* ---- LLaMA block pieces: RMSNorm, SwiGLU, rotary embedding ----------------------- */
+/* y = x * rstd * gamma, rstd = 1/sqrt(mean(x^2) + eps) (fp32 rstd out, [rows]) */
+int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols, float eps,
+                    uintptr_t stream);
+/* dx = rstd*(dy*g - xhat*mean(dy*g*xhat)) (+ dresid); dgamma (+)= sum_rows dy*xhat;
+ * workspace as for zpp_layernorm_bwd */
+int zpp_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, const void* gamma, const void* dresid,
+                    void* dx, float* dgamma, float* workspace, int rows, int cols, int accumulate, uintptr_t stream);
+/* gu [rows, 2*ffn] = [gate | up] -> a [rows, ffn] = silu(gate) * up; bwd -> dgu [rows, 2*ffn] */
+int zpp_swiglu_fwd(const void* gu, void* a, int rows, int ffn, uintptr_t stream);
+int zpp_swiglu_bwd(const void* da, const void* gu, void* dgu, int rows, int ffn, uintptr_t stream);
+/* in-place rotate-half RoPE of the q and k parts of qkv [tokens, 3, heads, head_dim];
+   position = token % seq; inverse = 1 applies the transpose (backward) */
+int zpp_rope(void* qkv, int tokens, int seq, int heads, int head_dim, float base, int inverse, uintptr_t stream);
+
 /* ---- bias gradient: dbias(f32)[c] += sum_r dy[r,c] (deterministic; = when accumulate == 0); workspace as for
  * zpp_layernorm_bwd (zero-initialised once, zpp_layernorm_bwd_workspace_floats(rows, cols)). */
 int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,

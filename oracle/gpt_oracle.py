@@ -20,7 +20,9 @@ reference's schedule implies:
   torch.optim.AdamW semantics on fp32 master weights.
 
 The model is the GPT-2 style pre-LN decoder the engine runs (untied LM head,
-tanh GeLU, causal attention, loss = mean token cross-entropy).
+tanh GeLU, causal attention, loss = mean token cross-entropy), or the LLaMA
+block of BASELINE config C4 (RMSNorm, SwiGLU, rotate-half RoPE, no biases, no
+learned positions; ``llama_forward_loss``).
 """
 
 from __future__ import annotations
@@ -58,14 +60,59 @@ def gpt_forward_loss(params: dict, ids: torch.Tensor, labels: torch.Tensor, *, l
     return F.cross_entropy(logits.view(N * s, -1), labels.reshape(-1))
 
 
+def _rms(x, g, eps):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * g
+
+
+def _rope(t, base: float):
+    """Rotate-half RoPE of t [N, H, s, d] at positions 0..s-1."""
+    s, d = t.shape[-2], t.shape[-1]
+    inv = torch.exp2(-(2.0 * torch.arange(d // 2, dtype=torch.float32) / d) * math.log2(base))
+    ang = torch.arange(s, dtype=torch.float32)[:, None] * inv[None]
+    cos, sin = ang.cos(), ang.sin()
+    a, b = t[..., : d // 2], t[..., d // 2:]
+    return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
+
+
+def llama_forward_loss(params: dict, ids: torch.Tensor, labels: torch.Tensor, *, layers: int, heads: int,
+                       eps: float = 1e-5, rope_base: float = 10000.0) -> torch.Tensor:
+    """LLaMA block (SURVEY.md C4): x += Wo attn(rope(q), rope(k), v)(rms(x));
+    x += Wdown (silu(gate) * up)(rms(x)) with [gate; up] = w_fc1 rms(x)."""
+    N, s = ids.shape
+    wte = params[("wte", None)]
+    h = wte.shape[1]
+    dh = h // heads
+    x = wte[ids]
+    mask = torch.ones(s, s, dtype=torch.bool).triu(1)
+    for l in range(layers):
+        p = lambda n: params[(n, l)]  # noqa: E731
+        qkv = _rms(x, p("ln1_g"), eps) @ p("w_qkv").t()
+        q, k, v = qkv.view(N, s, 3, heads, dh).unbind(2)
+        q, k, v = (t.transpose(1, 2) for t in (q, k, v))
+        q, k = _rope(q, rope_base), _rope(k, rope_base)
+        att = (q @ k.transpose(-1, -2)) / math.sqrt(dh)
+        att = att.masked_fill(mask, float("-inf")).softmax(-1)
+        o = (att @ v).transpose(1, 2).reshape(N, s, h)
+        x = x + o @ p("w_proj").t()
+        gate, up = (_rms(x, p("ln2_g"), eps) @ p("w_fc1").t()).chunk(2, dim=-1)
+        x = x + (F.silu(gate) * up) @ p("w_fc2").t()
+    xf = _rms(x, params[("lnf_g", None)], eps)
+    logits = xf @ params[("w_lm", None)].t()
+    return F.cross_entropy(logits.view(N * s, -1), labels.reshape(-1))
+
+
 def oracle_step(params: dict, ids: torch.Tensor, labels: torch.Tensor, *, layers: int, heads: int,
                 lr: float, betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1,
-                ln_eps: float = 1e-5, threads: int | None = None):
+                ln_eps: float = 1e-5, threads: int | None = None, arch: str = "gpt",
+                rope_base: float = 10000.0):
     """One step: returns (loss, grads dict, updated params dict), all fp32 CPU."""
     if threads:
         torch.set_num_threads(threads)
     leaf = {k: v.detach().clone().float().requires_grad_(True) for k, v in params.items()}
-    loss = gpt_forward_loss(leaf, ids, labels, layers=layers, heads=heads, eps=ln_eps)
+    if arch == "llama":
+        loss = llama_forward_loss(leaf, ids, labels, layers=layers, heads=heads, eps=ln_eps, rope_base=rope_base)
+    else:
+        loss = gpt_forward_loss(leaf, ids, labels, layers=layers, heads=heads, eps=ln_eps)
     loss.backward()
     grads = {k: v.grad.detach().clone() for k, v in leaf.items()}
     opt = torch.optim.AdamW(list(leaf.values()), lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,

@@ -40,6 +40,7 @@ from .simulation import (
     simulate,
 )
 from .render import RenderFormat, chrome_trace, render_timeline
+from .planner import PlanResult, PlanRow, SearchSpace, report, search, search_measured
 
 __version__ = "0.1.0"
 
@@ -52,6 +53,7 @@ __all__ = [
     "schedule_to_json", "validate", "__version__",
     "MemoryBreakdown", "SimResult", "SimulationDeadlock", "bubble_count", "comm_volume",
     "peak_memory", "simulate", "RenderFormat", "chrome_trace", "render_timeline",
+    "PlanResult", "PlanRow", "SearchSpace", "report", "search", "search_measured",
 ]
 
 

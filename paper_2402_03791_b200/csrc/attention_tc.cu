@@ -1,7 +1,10 @@
 // Causal flash-attention FORWARD on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
 // One CTA per (128-query block, batch*head); q-blocks scheduled latest-first.
-//   warp 0     TMA producer: Q once, then K/V 128-key tiles through a 2-stage ring
+//   warp 0     TMA producer: Q once, then K 128-key tiles through a 2-stage ring
+//   warp 3     TMA producer: V tiles through their own 2-stage ring.  K_i's slot frees as
+//              soon as S_i is computed, so K_{i+2} streams in while PV_i / softmax run
+//              (a joint K/V slot would put PV_i + the TMA latency on the S critical path)
 //   warp 1     MMA issuer (one lane):  S_i = Q K_i^T   (M=128, N=128, K=d)  -> TMEM S[i%2]
 //                                      O  += P_i V_i    (M=128, N=d,  K=128) -> TMEM O
 //              S_{i+1} is issued before O += P_i V_i so the tensor core works while
@@ -51,8 +54,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t bars = base + C::BAR_OFF;
-  const uint32_t q_full = bars, kv_full0 = bars + 8, kv_empty0 = bars + 24, s_full0 = bars + 40;
-  const uint32_t p_full = bars + 56, o_done = bars + 64;
+  const uint32_t q_full = bars, k_full0 = bars + 8, k_empty0 = bars + 24, s_full0 = bars + 40;
+  const uint32_t p_full = bars + 56, o_done = bars + 64, v_full0 = bars + 72, v_empty0 = bars + 88;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 128);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -66,8 +69,10 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(kv_full0 + 8 * s, 1);
-      mbar_init(kv_empty0 + 8 * s, 1);
+      mbar_init(k_full0 + 8 * s, 1);
+      mbar_init(k_empty0 + 8 * s, 1);
+      mbar_init(v_full0 + 8 * s, 1);
+      mbar_init(v_empty0 + 8 * s, 1);
       mbar_init(s_full0 + 8 * s, 1);
     }
     mbar_init(p_full, 128);
@@ -86,14 +91,24 @@ __global__ void __launch_bounds__(256, 1)
       for (int a = 0; a < NA; ++a) tma_load_2d(base + C::Q_OFF + a * C::ATOM, &tm_qkv, q_full, h * D + 64 * a, row_base + q0);
       for (int i = 0; i < nkb; ++i) {
         const int st = i & 1;
-        mbar_wait(kv_empty0 + 8 * st, ((i >> 1) & 1) ^ 1);
-        const uint32_t fb = kv_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, 2 * C::TILE);
-        for (int a = 0; a < NA; ++a) {
+        mbar_wait(k_empty0 + 8 * st, ((i >> 1) & 1) ^ 1);
+        const uint32_t fb = k_full0 + 8 * st;
+        mbar_arrive_expect_tx(fb, C::TILE);
+        for (int a = 0; a < NA; ++a)
           tma_load_2d(base + C::K_OFF + st * C::TILE + a * C::ATOM, &tm_qkv, fb, H * D + h * D + 64 * a, row_base + i * 128);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i & 1;
+        mbar_wait(v_empty0 + 8 * st, ((i >> 1) & 1) ^ 1);
+        const uint32_t fb = v_full0 + 8 * st;
+        mbar_arrive_expect_tx(fb, C::TILE);
+        for (int a = 0; a < NA; ++a)
           tma_load_2d(base + C::V_OFF + st * C::TILE + a * C::ATOM, &tm_qkv, fb, 2 * H * D + h * D + 64 * a,
                       row_base + i * 128);
-        }
       }
     }
     __syncwarp();
@@ -103,7 +118,7 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
       auto issue_s = [&](int i) {
         const int st = i & 1;
-        mbar_wait(kv_full0 + 8 * st, (i >> 1) & 1);
+        mbar_wait(k_full0 + 8 * st, (i >> 1) & 1);
         tc_fence_after();
         const uint32_t kb = base + C::K_OFF + st * C::TILE;
 #pragma unroll
@@ -113,12 +128,14 @@ __global__ void __launch_bounds__(256, 1)
                    kk > 0 ? 1u : 0u);
         }
         mma_commit(s_full0 + 8 * st);
+        mma_commit(k_empty0 + 8 * st);
       };
       mbar_wait(q_full, 0);
       issue_s(0);
       for (int i = 0; i < nkb; ++i) {
         if (i + 1 < nkb) issue_s(i + 1);
         mbar_wait(p_full, i & 1);
+        mbar_wait(v_full0 + 8 * (i & 1), (i >> 1) & 1);
         tc_fence_after();
         const uint32_t vb = base + C::V_OFF + (i & 1) * C::TILE;
 #pragma unroll
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(256, 1)
           mma_bf16(tmem + 256, ad, bd, idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(o_done);
-        mma_commit(kv_empty0 + 8 * (i & 1));
+        mma_commit(v_empty0 + 8 * (i & 1));
       }
     }
     __syncwarp();

@@ -1,5 +1,5 @@
-// HBM-bound kernels of the ZeroPP step: LayerNorm fwd/bwd, bias-grad column sums,
-// GeLU, embedding fwd/bwd, fused softmax cross-entropy, ZeRO grad cast/accumulate,
+// HBM-bound kernels of the ZeroPP step: LayerNorm / RMSNorm fwd/bwd, bias-grad column
+// sums, GeLU, SwiGLU fwd/bwd, rotary embedding, embedding fwd/bwd, fused softmax cross-entropy, ZeRO grad cast/accumulate,
 // sharded AdamW and the deterministic parameter initialiser.
 //
 // Every kernel moves 16-byte vectors, keeps fp32 statistics, and uses fixed-order
@@ -46,6 +46,8 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 // LayerNorm: one 256-thread block per row, row cached in registers (cols <= 8192).
 constexpr int LN_VPT = 4;  // uint4 (8 bf16) vectors per thread
 
+// RMS = true: RMSNorm (LLaMA): mean fixed at 0, no beta; mean_out may be null.
+template <bool RMS>
 __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
                                                             const bf16* __restrict__ b, bf16* __restrict__ y,
                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
       for (int j = 0; j < 8; ++j) s += v[i][j];
     }
   }
-  const float mean = block_sum256(s, red) / cols;
+  const float mean = RMS ? 0.f : block_sum256(s, red) / cols;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
@@ -81,22 +83,24 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
   for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * 256;
     if (vi < nvec) {
-      float gg[8], bb[8], o[8];
+      float gg[8], bb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
       unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg);
-      unpack8(*reinterpret_cast<const uint4*>(b + vi * 8), bb);
+      if (!RMS) unpack8(*reinterpret_cast<const uint4*>(b + vi * 8), bb);
 #pragma unroll
       for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mean) * rstd * gg[j] + bb[j];
       *reinterpret_cast<uint4*>(yr + vi * 8) = pack8(o);
     }
   }
   if (threadIdx.x == 0) {
-    mean_out[row] = mean;
+    if (!RMS) mean_out[row] = mean;
     rstd_out[row] = rstd;
   }
 }
 
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
-// the two row sums fused into a single float2 block reduction.
+// the two row sums fused into a single float2 block reduction.  RMS: mean = 0 and the
+// mean(dy*g) term drops (xhat = x * rstd).
+template <bool RMS>
 __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                                                const float* __restrict__ mean,
                                                                const float* __restrict__ rstd,
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __res
   __shared__ float2 red[8];
   const int row = blockIdx.x;
   const int nvec = cols / 8;
-  const float mu = mean[row], rs = rstd[row];
+  const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
   const bf16* xr = x + (long long)row * cols;
   const bf16* dyr = dy + (long long)row * cols;
   float xh[LN_VPT][8], dg[LN_VPT][8];
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __res
   float2 t = red[0];
 #pragma unroll
   for (int i = 1; i < 8; ++i) { t.x += red[i].x; t.y += red[i].y; }
-  const float m1 = t.x / cols, m2 = t.y / cols;
+  const float m1 = RMS ? 0.f : t.x / cols, m2 = t.y / cols;
   bf16* dxr = dx + (long long)row * cols;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
       if (LN) {
         float xv[8];
         unpack8(__ldcs(reinterpret_cast<const uint4*>(x + (long long)r * cols + c0)), xv);
-        const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+        const float mu = mean ? __ldg(mean + r) : 0.f, rs = __ldg(rstd + r);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           a0[j] += d[j] * (xv[j] - mu) * rs;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
     float sum = 0.f;
     for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(&ws[((long long)sp * NO + k) * ws_ld + col]);
     float* o = k == 0 ? out0 : out1;
-    o[col] = accumulate ? o[col] + sum : sum;
+    if (o) o[col] = accumulate ? o[col] + sum : sum;
   }
   if (threadIdx.x == 0) tickets[strip] = 0;  // re-arm for the next launch (stream-ordered)
 }
@@ -252,15 +256,94 @@ __global__ void gelu_kernel(const bf16* __restrict__ u, bf16* __restrict__ g, lo
 }
 
 // ----------------------------------------------------------------------------
-// Embedding: out[t] = wte[ids[t]] + wpe[t % seq]
+// SwiGLU (LLaMA MLP): gu [T, 2f] = [gate | up] -> a [T, f] = silu(gate) * up.
+// Backward: dgate = da * up * s * (1 + gate * (1 - s)), dup = da * silu(gate), s = sigmoid(gate).
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
+
+__global__ void swiglu_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ a, int f, long long nvec) {
+  const int fv = f / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / fv, c = i % fv;
+    const bf16* row = gu + t * 2 * f;
+    float g[8], u[8];
+    unpack8(reinterpret_cast<const uint4*>(row)[c], g);
+    unpack8(reinterpret_cast<const uint4*>(row + f)[c], u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] = g[j] * sigmoid_f(g[j]) * u[j];
+    reinterpret_cast<uint4*>(a)[i] = pack8(g);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const bf16* __restrict__ da, const bf16* __restrict__ gu, bf16* __restrict__ dgu,
+                                  int f, long long nvec) {
+  const int fv = f / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / fv, c = i % fv;
+    const bf16* row = gu + t * 2 * f;
+    float g[8], u[8], d[8], dg[8], du[8];
+    unpack8(reinterpret_cast<const uint4*>(row)[c], g);
+    unpack8(reinterpret_cast<const uint4*>(row + f)[c], u);
+    unpack8(reinterpret_cast<const uint4*>(da)[i], d);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float sg = sigmoid_f(g[j]);
+      du[j] = d[j] * g[j] * sg;
+      dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
+    }
+    bf16* orow = dgu + t * 2 * f;
+    reinterpret_cast<uint4*>(orow)[c] = pack8(dg);
+    reinterpret_cast<uint4*>(orow + f)[c] = pack8(du);
+  }
+}
+
+// Rotary position embedding (rotate-half convention) in place on the q and k parts of
+// qkv [T, 3, H, D]: for i < D/2, (x_i, x_{i+D/2}) rotates by angle pos * base^(-2i/D),
+// pos = t % seq.  inverse = 1 rotates by -angle (the backward of the forward rotation).
+// One thread per (token, q|k, head, 8-pair group): 16-byte loads of both halves.
+__global__ void rope_kernel(bf16* __restrict__ qkv, int seq, int H, int D, float log2_base, int inverse,
+                            long long nwork) {
+  const int hv = D / 16;  // 8-pair groups per head
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < nwork; w += (long long)gridDim.x * blockDim.x) {
+    const int grp = w % hv;
+    const long long th = w / hv;           // (token, part, head)
+    const int head = th % H;
+    const int part = (th / H) % 2;
+    const long long t = th / (2 * H);
+    bf16* base = qkv + t * 3 * H * D + (long long)part * H * D + (long long)head * D;
+    float lo[8], hi[8];
+    unpack8(reinterpret_cast<const uint4*>(base)[grp], lo);
+    unpack8(reinterpret_cast<const uint4*>(base + D / 2)[grp], hi);
+    const float pos = (float)(t % seq);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = grp * 8 + j;
+      const float inv_freq = exp2f(-(2.f * i / D) * log2_base);
+      float sn, cs;
+      sincosf(pos * inv_freq, &sn, &cs);
+      if (inverse) sn = -sn;
+      const float a = lo[j], b = hi[j];
+      lo[j] = a * cs - b * sn;
+      hi[j] = b * cs + a * sn;
+    }
+    reinterpret_cast<uint4*>(base)[grp] = pack8(lo);
+    reinterpret_cast<uint4*>(base + D / 2)[grp] = pack8(hi);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Embedding: out[t] = wte[ids[t]] + wpe[t % seq]  (wpe may be null: no learned positions)
 __global__ void embed_fwd_kernel(const int64_t* __restrict__ ids, const bf16* __restrict__ wte,
                                  const bf16* __restrict__ wpe, bf16* __restrict__ out, int seq, int hidden) {
   const int t = blockIdx.x;
   const long long id = ids[t];
   const bf16* e = wte + id * hidden;
-  const bf16* p = wpe + (long long)(t % seq) * hidden;
+  const bf16* p = wpe ? wpe + (long long)(t % seq) * hidden : nullptr;
   bf16* o = out + (long long)t * hidden;
   for (int v = threadIdx.x; v < hidden / 8; v += blockDim.x) {
+    if (!p) {
+      reinterpret_cast<uint4*>(o)[v] = reinterpret_cast<const uint4*>(e)[v];
+      continue;
+    }
     float a[8], b[8];
     unpack8(reinterpret_cast<const uint4*>(e)[v], a);
     unpack8(reinterpret_cast<const uint4*>(p)[v], b);
@@ -274,7 +357,7 @@ __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, const bf16* __
                                  float* __restrict__ dwte, float* __restrict__ dwpe, int seq, int hidden) {
   const int t = blockIdx.x;
   float* e = dwte + ids[t] * (long long)hidden;
-  float* p = dwpe + (long long)(t % seq) * hidden;
+  float* p = dwpe ? dwpe + (long long)(t % seq) * hidden : nullptr;
   const bf16* d = dout + (long long)t * hidden;
   for (int v = threadIdx.x; v < hidden / 8; v += blockDim.x) {
     float a[8];
@@ -282,7 +365,7 @@ __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, const bf16* __
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       atomicAdd(e + v * 8 + j, a[j]);
-      atomicAdd(p + v * 8 + j, a[j]);
+      if (p) atomicAdd(p + v * 8 + j, a[j]);
     }
   }
 }
@@ -426,7 +509,9 @@ static int grid_for(long long n, int per_block) {
 
 int kernels_preload() {
   cudaFuncAttributes fa;
-  const void* fns[] = {(const void*)layernorm_fwd_kernel, (const void*)layernorm_bwd_dx_kernel,
+  const void* fns[] = {(const void*)layernorm_fwd_kernel<false>, (const void*)layernorm_bwd_dx_kernel<false>,
+                       (const void*)layernorm_fwd_kernel<true>, (const void*)layernorm_bwd_dx_kernel<true>,
+                       (const void*)swiglu_fwd_kernel, (const void*)swiglu_bwd_kernel, (const void*)rope_kernel,
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_kernel,
                        (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel,
@@ -448,7 +533,7 @@ extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* b
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  layernorm_fwd_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
+  layernorm_fwd_kernel<false><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
                                                           (bf16*)y, mean, rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
@@ -482,12 +567,63 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  layernorm_bwd_dx_kernel<<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
+  layernorm_bwd_dx_kernel<false><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
                                                              (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc) return rc;
   return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, accumulate,
                        STREAM(stream));
+}
+
+extern "C" int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols, float eps,
+                               uintptr_t stream) {
+  if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm: cols % 8 != 0 or cols > 8192");
+  if (rows <= 0) return ZPP_OK;
+  layernorm_fwd_kernel<true><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y,
+                                                               nullptr, rstd, cols, eps);
+  return check_launch("rmsnorm_fwd");
+}
+
+extern "C" int zpp_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, const void* gamma,
+                               const void* dresid, void* dx, float* dgamma, float* workspace, int rows, int cols,
+                               int accumulate, uintptr_t stream) {
+  if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: cols % 8 != 0 or > 8192");
+  if (!workspace) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: workspace required");
+  if (rows <= 0) return ZPP_OK;
+  layernorm_bwd_dx_kernel<true><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, nullptr, rstd,
+                                                                  (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx,
+                                                                  cols);
+  int rc = check_launch("rmsnorm_bwd_dx");
+  if (rc) return rc;
+  return colred_launch(true, dy, cols, x, nullptr, rstd, dgamma, nullptr, workspace, rows, cols, accumulate,
+                       STREAM(stream));
+}
+
+extern "C" int zpp_swiglu_fwd(const void* gu, void* a, int rows, int ffn, uintptr_t stream) {
+  if (ffn % 8) return set_error(ZPP_ERR_ARG, "swiglu: ffn % 8 != 0");
+  const long long nvec = (long long)rows * ffn / 8;
+  if (nvec == 0) return ZPP_OK;
+  swiglu_fwd_kernel<<<grid_for(nvec, 256), 256, 0, STREAM(stream)>>>((const bf16*)gu, (bf16*)a, ffn, nvec);
+  return check_launch("swiglu_fwd");
+}
+
+extern "C" int zpp_swiglu_bwd(const void* da, const void* gu, void* dgu, int rows, int ffn, uintptr_t stream) {
+  if (ffn % 8) return set_error(ZPP_ERR_ARG, "swiglu_bwd: ffn % 8 != 0");
+  const long long nvec = (long long)rows * ffn / 8;
+  if (nvec == 0) return ZPP_OK;
+  swiglu_bwd_kernel<<<grid_for(nvec, 256), 256, 0, STREAM(stream)>>>((const bf16*)da, (const bf16*)gu, (bf16*)dgu,
+                                                                     ffn, nvec);
+  return check_launch("swiglu_bwd");
+}
+
+extern "C" int zpp_rope(void* qkv, int tokens, int seq, int heads, int head_dim, float base, int inverse,
+                        uintptr_t stream) {
+  if (head_dim % 16) return set_error(ZPP_ERR_ARG, "rope: head_dim % 16 != 0");
+  const long long nwork = (long long)tokens * 2 * heads * (head_dim / 16);
+  if (nwork == 0) return ZPP_OK;
+  rope_kernel<<<grid_for(nwork, 256), 256, 0, STREAM(stream)>>>((bf16*)qkv, seq, heads, head_dim, log2f(base),
+                                                                inverse, nwork);
+  return check_launch("rope");
 }
 
 extern "C" int zpp_colsum_acc(const void* dy, long long ld, float* dbias, float* workspace, int rows, int cols,

@@ -496,6 +496,8 @@ class Runtime:
 
     def _stage_layers(self, st: "_Stage", x: torch.Tensor):
         """Run the stage's transformer blocks on x; returns (per-layer stash, output)."""
+        if self.spec.llama:
+            return self._llama_layers(st, x)
         spec = self.spec
         T, h, H, dh = spec.tokens_per_microbatch, spec.hidden, spec.heads, spec.head_dim
         b, sl = spec.microbatch_samples, spec.seq_len
@@ -523,6 +525,60 @@ class Runtime:
             x = x2
         return layers, x
 
+    def _llama_layers(self, st: "_Stage", x: torch.Tensor):
+        """LLaMA blocks (RMSNorm, RoPE in place on q/k, SwiGLU; no biases)."""
+        spec = self.spec
+        T, h, H, dh, f = spec.tokens_per_microbatch, spec.hidden, spec.heads, spec.head_dim, spec.ffn
+        b, sl = spec.microbatch_samples, spec.seq_len
+        P = st.p
+        e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
+        layers = []
+        lo, hi = st.lay.layers
+        for l in range(lo, hi):
+            xn1, r1 = e(T, h), e(T, dt=F32)
+            ops.rmsnorm_fwd(x, P[("ln1_g", l)], xn1, r1, spec.ln_eps)
+            qkv = e(T, 3 * h)
+            ops.gemm(xn1, P[("w_qkv", l)], qkv)
+            ops.rope(qkv, sl, H, dh, spec.rope_base)
+            o, lse = e(T, h), e(b, H, sl, dt=F32)
+            ops.attn_fwd(qkv, o, lse, b, sl, H, dh)
+            x1 = e(T, h)
+            ops.gemm(o, P[("w_proj", l)], x1, resid=x)
+            xn2, r2 = e(T, h), e(T, dt=F32)
+            ops.rmsnorm_fwd(x1, P[("ln2_g", l)], xn2, r2, spec.ln_eps)
+            gu, a = e(T, 2 * f), e(T, f)
+            ops.gemm(xn2, P[("w_fc1", l)], gu)
+            ops.swiglu_fwd(gu, a)
+            x2 = e(T, h)
+            ops.gemm(a, P[("w_fc2", l)], x2, resid=x1)
+            layers.append({"x": x, "xn1": xn1, "r1": r1, "qkv": qkv, "o": o, "lse": lse,
+                           "x1": x1, "xn2": xn2, "r2": r2, "gu": gu, "a": a})
+            x = x2
+        return layers, x
+
+    def _final_norm(self, st: "_Stage", out: torch.Tensor):
+        spec, P = self.spec, st.p
+        T, h = out.shape
+        xf, rf = torch.empty(T, h, dtype=BF16, device=self.dev), torch.empty(T, dtype=F32, device=self.dev)
+        if spec.llama:
+            ops.rmsnorm_fwd(out, P[("lnf_g", None)], xf, rf, spec.ln_eps)
+            return xf, {"xlast": out, "rf": rf}
+        muf = torch.empty(T, dtype=F32, device=self.dev)
+        ops.layernorm_fwd(out, P[("lnf_g", None)], P[("lnf_b", None)], xf, muf, rf, spec.ln_eps)
+        return xf, {"xlast": out, "muf": muf, "rf": rf}
+
+    def _final_norm_bwd(self, st: "_Stage", stash: dict, dxf: torch.Tensor) -> torch.Tensor:
+        P, G = st.p, st.g
+        dx = torch.empty_like(dxf)
+        if self.spec.llama:
+            ops.rmsnorm_bwd(dxf, stash.pop("xlast"), stash.pop("rf"), P[("lnf_g", None)], dx, G[("lnf_g", None)],
+                            self.ln_ws, accumulate=st.accumulate(("lnf_g", None)))
+            return dx
+        ops.layernorm_bwd(dxf, stash.pop("xlast"), stash.pop("muf"), stash.pop("rf"), P[("lnf_g", None)], dx,
+                          G[("lnf_g", None)], G[("lnf_b", None)], self.ln_ws,
+                          accumulate=st.accumulate(("lnf_g", None)) | st.accumulate(("lnf_b", None)))
+        return dx
+
     def _forward(self, s: int, m: int) -> None:
         spec = self.spec
         st = self.stages[s]
@@ -532,7 +588,7 @@ class Runtime:
         e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
         if s == 0:
             x = e(T, h)
-            ops.embed_fwd(self._ids[m], P[("wte", None)], P[("wpe", None)], x, spec.seq_len)
+            ops.embed_fwd(self._ids[m], P[("wte", None)], P.get(("wpe", None)), x, spec.seq_len)
         elif self._dev_of(s - 1) == self.p:
             x = self._local_act.pop((s, m))
         else:
@@ -544,12 +600,11 @@ class Runtime:
         else:
             stash = {"layers": layers}
         if s == self.S - 1:
-            xf, muf, rf = e(T, h), e(T, dt=F32), e(T, dt=F32)
-            ops.layernorm_fwd(out, P[("lnf_g", None)], P[("lnf_b", None)], xf, muf, rf, spec.ln_eps)
+            xf, norm_stash = self._final_norm(st, out)
             logits = e(T, spec.vocab)
             ops.gemm(xf, P[("w_lm", None)], logits)
             ops.xent(logits, self._labels[m], self.loss_sum, self._grad_scale)
-            stash.update(xlast=out, xf=xf, muf=muf, rf=rf, dlogits=logits)
+            stash.update(norm_stash, xf=xf, dlogits=logits)
         elif self._dev_of(s + 1) == self.p:
             self._local_act[(s + 1, m)] = out
         else:
@@ -577,17 +632,16 @@ class Runtime:
         if s == self.S - 1:
             dxf = e(T, h)
             ops.gemm(stash["dlogits"], P[("w_lm", None)], dxf, b_t=True)
-            dx = e(T, h)
-            ops.layernorm_bwd(dxf, stash["xlast"], stash["muf"], stash["rf"], P[("lnf_g", None)], dx,
-                              G[("lnf_g", None)], G[("lnf_b", None)], self.ln_ws,
-                              accumulate=st.accumulate(("lnf_g", None)) | st.accumulate(("lnf_b", None)))
-            del stash["xlast"], stash["muf"], stash["rf"]
+            dx = self._final_norm_bwd(st, stash, dxf)
         elif self._dev_of(s + 1) == self.p:
             dx = self._local_grad.pop((s, m))
         else:
             dx = self._recv("grad", (T, h), self._dev_of(s + 1))
         lo, hi = st.lay.layers
         for i, l in reversed(list(enumerate(range(lo, hi)))):
+            if spec.llama:
+                dx = self._llama_layer_bwd(st, stash["layers"], i, l, dx)
+                continue
             a = stash["layers"][i]
             d2 = dx
             du = e(T, 4 * h)
@@ -619,24 +673,60 @@ class Runtime:
         else:
             self._send("grad", dx, self._dev_of(s - 1))
 
+    def _llama_layer_bwd(self, st: "_Stage", layers: list, i: int, l: int, dx: torch.Tensor) -> torch.Tensor:
+        """Input-gradient of one LLaMA block; leaves what W needs in ``layers[i]``."""
+        spec = self.spec
+        T, h, H, dh, f = spec.tokens_per_microbatch, spec.hidden, spec.heads, spec.head_dim, spec.ffn
+        b, sl = spec.microbatch_samples, spec.seq_len
+        P, G = st.p, st.g
+        e = lambda *shape, dt=BF16: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
+        a = layers[i]
+        d2 = dx
+        da = e(T, f)
+        ops.gemm(d2, P[("w_fc2", l)], da, b_t=True)
+        dgu = e(T, 2 * f)
+        ops.swiglu_bwd(da, a["gu"], dgu)
+        dxn2 = e(T, h)
+        ops.gemm(dgu, P[("w_fc1", l)], dxn2, b_t=True)
+        dx1 = e(T, h)
+        ops.rmsnorm_bwd(dxn2, a["x1"], a["r2"], P[("ln2_g", l)], dx1, G[("ln2_g", l)], self.ln_ws, dresid=d2,
+                        accumulate=st.accumulate(("ln2_g", l)))
+        do = e(T, h)
+        ops.gemm(dx1, P[("w_proj", l)], do, b_t=True)
+        dqkv = e(T, 3 * h)
+        ops.attn_bwd(a["qkv"], a["o"], a["lse"], do, dqkv, self.attn_ws, b, sl, H, dh)
+        ops.rope(dqkv, sl, H, dh, spec.rope_base, inverse=True)   # d(pre-rotation q, k)
+        dxn1 = e(T, h)
+        ops.gemm(dqkv, P[("w_qkv", l)], dxn1, b_t=True)
+        dxl = e(T, h)
+        ops.rmsnorm_bwd(dxn1, a["x"], a["r1"], P[("ln1_g", l)], dxl, G[("ln1_g", l)], self.ln_ws, dresid=dx1,
+                        accumulate=st.accumulate(("ln1_g", l)))
+        layers[i] = {"xn1": a["xn1"], "o": a["o"], "xn2": a["xn2"], "a": a["a"],
+                     "d2": d2, "dgu": dgu, "dx1": dx1, "dqkv": dqkv}
+        return dxl
+
     def _backward_weight(self, s: int, m: int) -> None:
         st = self.stages[s]
         self._touch_grads(st)
         G = st.g
         stash = self._stash.pop((s, m))
         lo, hi = st.lay.layers
+        linears = ((("d2", "a", "w_fc2", None), ("dgu", "xn2", "w_fc1", None), ("dx1", "o", "w_proj", None),
+                    ("dqkv", "xn1", "w_qkv", None)) if self.spec.llama else
+                   (("d2", "g", "w_fc2", "b_fc2"), ("du", "xn2", "w_fc1", "b_fc1"),
+                    ("dx1", "o", "w_proj", "b_proj"), ("dqkv", "xn1", "w_qkv", "b_qkv")))
         for i, l in enumerate(range(lo, hi)):
             a = stash["layers"][i]
-            for dy, x, w, bias in (("d2", "g", "w_fc2", "b_fc2"), ("du", "xn2", "w_fc1", "b_fc1"),
-                                   ("dx1", "o", "w_proj", "b_proj"), ("dqkv", "xn1", "w_qkv", "b_qkv")):
+            for dy, x, w, bias in linears:
                 ops.gemm(a[dy], a[x], G[(w, l)], a_t=True, b_t=True,
                          epilogue=ops.EPI_F32_ACC if st.accumulate((w, l)) else ops.EPI_F32)
-                ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws, accumulate=st.accumulate((bias, l)))
+                if bias is not None:
+                    ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws, accumulate=st.accumulate((bias, l)))
         if s == self.S - 1:
             ops.gemm(stash["dlogits"], stash["xf"], G[("w_lm", None)], a_t=True, b_t=True,
                      epilogue=ops.EPI_F32_ACC if st.accumulate(("w_lm", None)) else ops.EPI_F32)
         if s == 0:
-            ops.embed_bwd(self._ids[m], stash["demb"], G[("wte", None)], G[("wpe", None)],
+            ops.embed_bwd(self._ids[m], stash["demb"], G[("wte", None)], G.get(("wpe", None)),
                           self.spec.seq_len)
 
 

@@ -33,6 +33,11 @@ _SIGS = {
     "zpp_layernorm_fwd": (c_int, [P, P, P, P, P, P, c_int, c_int, c_float, c_stream]),
     "zpp_layernorm_bwd": (c_int, [P, P, P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_layernorm_bwd_workspace_floats": (c_longlong, [c_int, c_int]),
+    "zpp_rmsnorm_fwd": (c_int, [P, P, P, P, c_int, c_int, c_float, c_stream]),
+    "zpp_rmsnorm_bwd": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
+    "zpp_swiglu_fwd": (c_int, [P, P, c_int, c_int, c_stream]),
+    "zpp_swiglu_bwd": (c_int, [P, P, P, c_int, c_int, c_stream]),
+    "zpp_rope": (c_int, [P, c_int, c_int, c_int, c_int, c_float, c_int, c_stream]),
     "zpp_colsum_acc": (c_int, [P, c_size, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_gelu_fwd": (c_int, [P, P, c_size, c_stream]),
     "zpp_embed_fwd": (c_int, [P, P, P, P, c_int, c_int, c_int, c_stream]),

@@ -1,4 +1,5 @@
-"""GPT model description and the flat, ZeRO-shardable parameter layout of a stage.
+"""Model description (GPT or LLaMA block) and the flat, ZeRO-shardable parameter
+layout of a stage.
 
 The reference models a stage only as ``layers * M_w`` bytes (ModelSpec,
 `config.py:36-89`; stage bytes `schedules.py:45-49`).  The engine needs the
@@ -12,6 +13,11 @@ Layout of stage s with layers [lo, hi) (each tensor 64-element aligned):
     per layer: ln1_g, ln1_b, w_qkv [3h, h], b_qkv, w_proj [h, h], b_proj,
                ln2_g, ln2_b, w_fc1 [4h, h], b_fc1, w_fc2 [h, 4h], b_fc2
     s == S-1 : lnf_g, lnf_b, w_lm [V, h]
+LLaMA (``arch="llama"``: RMSNorm, SwiGLU, RoPE, no biases):
+    s == 0   : wte [V, h]
+    per layer: ln1_g, w_qkv [3h, h], w_proj [h, h], ln2_g, w_fc1 [2f, h] (= [gate; up]),
+               w_fc2 [h, f]
+    s == S-1 : lnf_g, w_lm [V, h]
 The flat size is padded to a multiple of 64*D (64*D*n in ZeRO-1 outer mode) so every
 ZeRO shard (and optimizer sub-shard) is 128-byte aligned.  Shard z of D owns elements
 [z*n/D, (z+1)*n/D).
@@ -26,6 +32,8 @@ ALIGN = 64
 
 LAYER_TENSORS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_proj", "b_proj",
                  "ln2_g", "ln2_b", "w_fc1", "b_fc1", "w_fc2", "b_fc2")
+LLAMA_LAYER_TENSORS = ("ln1_g", "w_qkv", "w_proj", "ln2_g", "w_fc1", "w_fc2")
+ARCHS = ("gpt", "llama")
 
 
 @dataclass(frozen=True)
@@ -47,8 +55,15 @@ class GPTSpec:
     beta2: float = 0.95
     adam_eps: float = 1e-8
     weight_decay: float = 0.1
+    arch: str = "gpt"                # "gpt" (pre-LN, GeLU, learned positions) | "llama"
+    ffn_hidden: int | None = None    # MLP width; default 4h (GPT)
+    rope_base: float = 10000.0       # LLaMA rotary base
 
     def __post_init__(self):
+        if self.arch not in ARCHS:
+            raise ValueError(f"arch must be one of {ARCHS}")
+        if self.ffn % 64:
+            raise ValueError("ffn_hidden must be a multiple of 64")
         if self.hidden % self.heads:
             raise ValueError("hidden must be divisible by heads")
         if self.head_dim not in (64, 128):
@@ -62,7 +77,11 @@ class GPTSpec:
 
     @property
     def ffn(self) -> int:
-        return 4 * self.hidden
+        return self.ffn_hidden or 4 * self.hidden
+
+    @property
+    def llama(self) -> bool:
+        return self.arch == "llama"
 
     @property
     def tokens_per_microbatch(self) -> int:
@@ -71,10 +90,14 @@ class GPTSpec:
     def flops_per_token(self) -> float:
         """Model FLOPs per token (fwd+bwd, attention at full s^2)."""
         L, h, s, V = self.num_layers, self.hidden, self.seq_len, self.vocab
+        if self.llama:
+            return 6.0 * L * (4.0 * h * h + 3.0 * h * self.ffn) + 12.0 * L * s * h + 6.0 * h * V
         return 72.0 * L * h * h + 12.0 * L * s * h + 6.0 * h * V
 
     def num_params(self) -> int:
         h, L, V, S = self.hidden, self.num_layers, self.vocab, self.seq_len
+        if self.llama:
+            return L * (4 * h * h + 3 * h * self.ffn + 2 * h) + V * h + h + V * h
         per_layer = 12 * h * h + 13 * h
         return L * per_layer + V * h + S * h + 2 * h + V * h
 
@@ -89,6 +112,17 @@ class GPTSpec:
     @classmethod
     def tiny(cls, **kw) -> "GPTSpec":
         return cls(num_layers=4, hidden=256, heads=4, seq_len=128, **kw)
+
+    @classmethod
+    def llama_7b(cls, **kw) -> "GPTSpec":
+        """L32 h4096 a32 s4096, SwiGLU ffn 11008, vocab 32000, RoPE, untied."""
+        return cls(num_layers=32, hidden=4096, heads=32, seq_len=4096, vocab=32000, arch="llama",
+                   ffn_hidden=11008, **kw)
+
+    @classmethod
+    def tiny_llama(cls, **kw) -> "GPTSpec":
+        return cls(num_layers=4, hidden=256, heads=4, seq_len=128, vocab=32000, arch="llama",
+                   ffn_hidden=704, **kw)
 
 
 @dataclass(frozen=True)
@@ -140,6 +174,26 @@ def stage_layout(spec: GPTSpec, stage: int, num_stages: int, layer_range: tuple[
         lay.slots.append(slot)
         off = _align(off + slot.numel)
 
+    if spec.llama:
+        f = spec.ffn
+        if stage == 0:
+            add("wte", None, (V, h), 1, sd=std)
+        for l in range(*layer_range):
+            base = 16 + 16 * l
+            shapes = {"ln1_g": (h,), "w_qkv": (3 * h, h), "w_proj": (h, h), "ln2_g": (h,),
+                      "w_fc1": (2 * f, h), "w_fc2": (h, f)}
+            for name in LLAMA_LAYER_TENSORS:
+                uid = base + LAYER_TENSORS.index(name)
+                if name.endswith("_g"):
+                    add(name, l, shapes[name], uid, mean=1.0)
+                else:
+                    add(name, l, shapes[name], uid, sd=proj_std if name in ("w_proj", "w_fc2") else std)
+        if stage == num_stages - 1:
+            add("lnf_g", None, (h,), 3, mean=1.0)
+            add("w_lm", None, (V, h), 5, sd=std)
+        lay.numel = _align(off, ALIGN * dp * sub)
+        lay.shard_numel = lay.numel // dp
+        return lay
     if stage == 0:
         add("wte", None, (V, h), 1, sd=std)
         add("wpe", None, (spec.seq_len, h), 2, sd=std)

@@ -21,6 +21,7 @@ class _Profile:
         self.time_gemms = True
         self.launches = 0
         self._gemms: list = []
+        self.shapes: list | None = None   # set to [] to log (M, N, K, algorithmic bytes) per GEMM
 
     def start(self, time_gemms: bool = True) -> None:
         self.active, self.launches, self._gemms = True, 0, []
@@ -82,6 +83,10 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_t: bool = False
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(ts)
         PROFILE._gemms.append((2.0 * M * N * K, e0, e1))
+    if PROFILE.shapes is not None:
+        out_bytes = c.element_size() * (2 if epilogue == EPI_F32_ACC else 1)
+        extra = (resid is not None) + (aux is not None)  # residual read; GeLU pre-act write / dGeLU read
+        PROFILE.shapes.append((M, N, K, 2 * (M * K + N * K) + M * N * (out_bytes + 2 * extra)))
     _count(1)
     return c
 
@@ -119,6 +124,40 @@ def layernorm_bwd(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, workspace, dresid
     _count(2)
     lib.call("zpp_layernorm_bwd", _p(dy), _p(x), _p(mean), _p(rstd), _p(gamma), _p(dresid), _p(dx),
              _p(dgamma), _p(dbeta), _p(workspace), rows, cols, int(accumulate), _s(stream))
+
+
+def rmsnorm_fwd(x, gamma, y, rstd, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    _count(1)
+    lib.call("zpp_rmsnorm_fwd", _p(x), _p(gamma), _p(y), _p(rstd), rows, cols, eps, _s(stream))
+
+
+def rmsnorm_bwd(dy, x, rstd, gamma, dx, dgamma, workspace, dresid=None, accumulate=True, stream=None):
+    """dgamma += column sums of dy * xhat, or = when ``accumulate`` is False (first writer)."""
+    rows, cols = x.shape
+    _count(2)
+    lib.call("zpp_rmsnorm_bwd", _p(dy), _p(x), _p(rstd), _p(gamma), _p(dresid), _p(dx), _p(dgamma),
+             _p(workspace), rows, cols, int(accumulate), _s(stream))
+
+
+def swiglu_fwd(gu, a, stream=None):
+    rows, ffn = a.shape
+    assert gu.shape == (rows, 2 * ffn)
+    _count(1)
+    lib.call("zpp_swiglu_fwd", _p(gu), _p(a), rows, ffn, _s(stream))
+
+
+def swiglu_bwd(da, gu, dgu, stream=None):
+    rows, ffn = da.shape
+    assert gu.shape == dgu.shape == (rows, 2 * ffn)
+    _count(1)
+    lib.call("zpp_swiglu_bwd", _p(da), _p(gu), _p(dgu), rows, ffn, _s(stream))
+
+
+def rope(qkv, seq, heads, head_dim, base=10000.0, inverse=False, stream=None):
+    """In-place rotary embedding of the q and k parts of qkv [tokens, 3*heads*head_dim]."""
+    _count(1)
+    lib.call("zpp_rope", _p(qkv), qkv.shape[0], seq, heads, head_dim, base, int(inverse), _s(stream))
 
 
 def colsum_acc(dy, dbias, workspace, accumulate=True, stream=None):

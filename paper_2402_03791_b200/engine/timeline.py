@@ -33,9 +33,8 @@ __all__ = ["measured_result", "calibrate", "predict", "model_flops_per_token"]
 
 
 def model_flops_per_token(spec) -> float:
-    """GPT model FLOPs per token, attention at full s^2."""
-    L, h, s, V = spec.num_layers, spec.hidden, spec.seq_len, spec.vocab
-    return 72.0 * L * h * h + 12.0 * L * s * h + 6.0 * h * V
+    """Model FLOPs per token (GPT or LLaMA), attention at full s^2."""
+    return spec.flops_per_token()
 
 
 def measured_result(runtime, res, gather: bool = True, peak_flops: float = 2.25e15) -> SimResult:

@@ -78,7 +78,8 @@ def oracle_for(spec, cfg, pl, tokens_step):
     params = oracle_params(spec, cfg, pl)
     return oracle_step(params, ids, labels, layers=spec.num_layers, heads=spec.heads, lr=spec.lr,
                        betas=(spec.beta1, spec.beta2), eps=spec.adam_eps,
-                       weight_decay=spec.weight_decay, ln_eps=spec.ln_eps)
+                       weight_decay=spec.weight_decay, ln_eps=spec.ln_eps, arch=spec.arch,
+                       rope_base=spec.rope_base)
 
 
 def compare_shards(spec, cfg, pl, rt, grads_o, new_o) -> list[str]:

@@ -44,6 +44,20 @@ def test_recompute_step_matches_oracle(B, U, V):
     assert not compare_shards(spec, cfg, pl, rt, grads_o, new_o)
 
 
+@pytest.mark.parametrize("B,U,V,recompute", [(4, 2, 2, False), (8, 4, 2, True), (4, 4, 1, False)])
+def test_llama_step_matches_oracle(B, U, V, recompute):
+    """LLaMA block (RMSNorm, SwiGLU, RoPE, no biases) through the same ZeroPP step."""
+    from paper_2402_03791_b200 import RecomputeMode
+    spec = GPTSpec.tiny_llama()
+    kw = {"recompute": RecomputeMode.FULL} if recompute else {}
+    rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, 1, 1, B, U, V, **kw)
+    loss = res[0].loss_sum.item() / (B * spec.tokens_per_microbatch)
+    loss_o, grads_o, new_o = oracle_for(spec, cfg, pl, tokens[0])
+    assert abs(loss - loss_o) / loss_o <= LOSS_RTOL, (loss, loss_o)
+    fails = compare_shards(spec, cfg, pl, rt, grads_o, new_o)
+    assert not fails, fails
+
+
 def test_measured_timeline_is_a_sim_result():
     """execute() with a timeline runtime returns the SimResult superset."""
     from paper_2402_03791_b200 import render_timeline

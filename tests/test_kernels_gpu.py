@@ -174,6 +174,66 @@ def test_layernorm(cols):
     assert rel_err(db, bff.grad) < 1e-4
 
 
+@pytest.mark.parametrize("cols", [256, 4096, 5120])
+def test_rmsnorm(cols):
+    """LLaMA RMSNorm fwd/bwd (dgamma overwrite and accumulate) vs fp32 torch."""
+    rows = 300
+    x = bf(rows, cols, scale=2.0) + 0.5
+    g = bf(cols) + 1.0
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, device=dev)
+    ops.rmsnorm_fwd(x, g, y, rstd)
+    xf = x.float().requires_grad_(True)
+    gf = g.float().requires_grad_(True)
+    yr = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5) * gf
+    assert rel_err(y, yr) < 1e-2
+    dy, dres = bf(rows, cols), bf(rows, cols)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.full((cols,), 5.0, device=dev)
+    ws = torch.zeros(ops.layernorm_bwd_workspace(rows, cols), device=dev)
+    ops.rmsnorm_bwd(dy, x, rstd, g, dx, dg, ws, dresid=dres, accumulate=False)
+    assert rel_err(dx, xf.grad + dres.float()) < 1e-2
+    assert rel_err(dg, gf.grad) < 1e-4
+    ops.rmsnorm_bwd(dy, x, rstd, g, dx, dg, ws, dresid=dres, accumulate=True)
+    assert rel_err(dg, 2 * gf.grad) < 1e-4
+
+
+@pytest.mark.parametrize("rows,ffn", [(300, 704), (2048, 11008)])
+def test_swiglu(rows, ffn):
+    gu = bf(rows, 2 * ffn, scale=2.0)
+    a = torch.empty(rows, ffn, dtype=torch.bfloat16, device=dev)
+    ops.swiglu_fwd(gu, a)
+    guf = gu.float().requires_grad_(True)
+    gate, up = guf.chunk(2, dim=-1)
+    ar = torch.nn.functional.silu(gate) * up
+    assert rel_err(a, ar) < 1e-2
+    da = bf(rows, ffn)
+    ar.backward(da.float())
+    dgu = torch.empty_like(gu)
+    ops.swiglu_bwd(da, gu, dgu)
+    assert rel_err(dgu, guf.grad) < 1e-2
+
+
+@pytest.mark.parametrize("b,s,H,D", [(2, 128, 4, 64), (1, 4096, 32, 128)])
+def test_rope(b, s, H, D):
+    """Rotate-half RoPE in place on q and k of qkv; v untouched; inverse undoes it."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.gpt_oracle import _rope
+    qkv = bf(b * s, 3 * H * D)
+    orig = qkv.clone()
+    ops.rope(qkv, s, H, D)
+    t = orig.float().cpu().view(b, s, 3, H, D)
+    ref_q = _rope(t[:, :, 0].transpose(1, 2), 10000.0).transpose(1, 2)
+    ref_k = _rope(t[:, :, 1].transpose(1, 2), 10000.0).transpose(1, 2)
+    got = qkv.float().cpu().view(b, s, 3, H, D)
+    assert rel_err(got[:, :, 0], ref_q) < 1e-2 and rel_err(got[:, :, 1], ref_k) < 1e-2
+    assert torch.equal(got[:, :, 2], t[:, :, 2])
+    ops.rope(qkv, s, H, D, inverse=True)
+    assert rel_err(qkv, orig.float()) < 1e-2
+
+
 @pytest.mark.parametrize("rows,cols", [(1000, 768), (2048, 16384), (64, 96)])
 def test_colsum(rows, cols):
     dy = bf(rows, cols)

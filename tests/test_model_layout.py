@@ -1,0 +1,55 @@
+"""Model descriptions on CPU: flat stage layouts cover exactly the model's parameters
+(GPT and LLaMA), shards / optimizer sub-shards are 128-byte aligned, and the fp32
+oracle runs both block types."""
+
+import math
+
+import pytest
+import torch
+
+from oracle.gpt_oracle import make_tokens, oracle_step
+from paper_2402_03791_b200 import ModelSpec, ParallelConfig, make_placement
+from paper_2402_03791_b200.engine import GPTSpec, stage_layout
+
+
+@pytest.mark.parametrize("spec", [GPTSpec.tiny(), GPTSpec.gpt_6p2b(), GPTSpec.tiny_llama(), GPTSpec.llama_7b()],
+                         ids=["gpt-tiny", "gpt-6.2b", "llama-tiny", "llama-7b"])
+@pytest.mark.parametrize("P,V,D,sub", [(1, 1, 1, 1), (2, 2, 4, 1), (4, 1, 2, 2)])
+def test_layout_covers_model(spec, P, V, D, sub):
+    model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
+    cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=P, unit_size=P, stages_per_device=V)
+    pl = make_placement(cfg, model)
+    total = 0
+    for s in range(cfg.num_stages):
+        lay = stage_layout(spec, s, cfg.num_stages, pl.stage_to_layers[s], D, sub)
+        total += sum(sl.numel for sl in lay.slots)
+        assert lay.numel % (64 * D * sub) == 0 and lay.shard_numel * D == lay.numel
+        assert all(sl.offset % 64 == 0 for sl in lay.slots)
+        ends = sorted((sl.offset, sl.offset + sl.numel) for sl in lay.slots)
+        assert all(a[1] <= b[0] for a, b in zip(ends, ends[1:]))
+    assert total == spec.num_params()
+
+
+def test_llama_7b_shape():
+    spec = GPTSpec.llama_7b()
+    assert 6.7e9 < spec.num_params() < 6.8e9
+    assert spec.flops_per_token() == pytest.approx(6 * 32 * (4 * 4096 ** 2 + 3 * 4096 * 11008)
+                                                   + 12 * 32 * 4096 * 4096 + 6 * 4096 * 32000)
+
+
+@pytest.mark.parametrize("arch", ["gpt", "llama"])
+def test_oracle_step_runs(arch):
+    import dataclasses
+    spec = dataclasses.replace(GPTSpec.tiny_llama() if arch == "llama" else GPTSpec.tiny(), num_layers=2)
+    g = torch.Generator().manual_seed(0)
+    model = ModelSpec(num_layers=2, hidden_size=spec.hidden, seq_len=spec.seq_len)
+    cfg = ParallelConfig(pp_size=1, dp_size=1, microbatches=1, unit_size=1)
+    pl = make_placement(cfg, model)
+    lay = stage_layout(spec, 0, 1, pl.stage_to_layers[0], 1)
+    params = {(sl.name, sl.layer): (torch.randn(*sl.shape, generator=g) * sl.std + sl.mean) for sl in lay.slots}
+    tok = make_tokens(1, 1, 1, 1, spec.seq_len, spec.vocab)[0, 0, :, 0]
+    loss, grads, new = oracle_step(params, tok[:, :-1], tok[:, 1:], layers=2, heads=spec.heads, lr=1e-3,
+                                   arch=arch)
+    assert abs(loss - math.log(spec.vocab)) < 0.5
+    assert set(grads) == set(params) and all(torch.isfinite(v).all() for v in grads.values())
+    assert all(not torch.equal(new[k], params[k]) for k in params)

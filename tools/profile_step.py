@@ -17,6 +17,7 @@ ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--B", type=int, default=8)
 ap.add_argument("--U", type=int, default=2)
 ap.add_argument("--ncu", action="store_true")
+ap.add_argument("--gemm-shapes", default=None, help="with --ncu: write M,N,K,algorithmic bytes per GEMM launch")
 a = ap.parse_args()
 spec = GPTSpec(num_layers=a.layers, hidden=4096, heads=32, seq_len=2048)
 model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
@@ -31,10 +32,17 @@ for _ in range(2):
     rt.step(ids, lab)
 torch.cuda.synchronize()
 if a.ncu:
+    from paper_2402_03791_b200.engine import ops
+    if a.gemm_shapes:
+        ops.PROFILE.shapes = []
     torch.cuda.profiler.start()
     rt.step(ids, lab)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
+    if a.gemm_shapes:
+        with open(a.gemm_shapes, "w") as f:
+            for row in ops.PROFILE.shapes:
+                f.write(",".join(map(str, row)) + "\n")
     sys.exit(0)
 from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
