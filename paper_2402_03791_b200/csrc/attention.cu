@@ -233,8 +233,10 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const bf16* __restrict__ 
 
 // delta[bh][t] = sum_d dO[t,h,d] * O[t,h,d]; one warp per (t, h)
 template <int D>
+// delta[b,h,t] = sum_d out*dout; also zeroes the fp32 dQ accumulator row it owns (the
+// backward kernels reduce-add into it), so no separate memset is launched.
 __global__ void attn_delta_kernel(const bf16* __restrict__ out, const bf16* __restrict__ dout,
-                                  float* __restrict__ delta, int B, int T, int H) {
+                                  float* __restrict__ delta, float* __restrict__ dq, int B, int T, int H) {
   const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (long long)B * T * H) return;
@@ -251,6 +253,8 @@ __global__ void attn_delta_kernel(const bf16* __restrict__ out, const bf16* __re
 #pragma unroll
   for (int x = 16; x > 0; x >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, x);
   if (lane == 0) delta[((long long)b * H + h) * T + t] = acc;
+  float4* z = reinterpret_cast<float4*>(dq + w * D);
+  for (int i = lane; i < D / 4; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // ---------------------------------------------------------------------------
@@ -467,11 +471,9 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
   float* delta = ws;
   float* dq = ws + (long long)B * H * T;
   const long long nrows = (long long)B * T;
-  cudaError_t e = cudaMemsetAsync(dq, 0, sizeof(float) * nrows * H * D, s);
-  if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd memset");
   const long long warps = nrows * H;
-  attn_delta_kernel<D><<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>((const bf16*)out, (const bf16*)dout, delta, B,
-                                                                      T, H);
+  attn_delta_kernel<D><<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>((const bf16*)out, (const bf16*)dout, delta, dq,
+                                                                      B, T, H);
   int rc = check_launch("attn_delta");
   if (rc) return rc;
   if (use_tc) {

@@ -46,8 +46,13 @@ struct TcFwdCfg {
 template <int D>
 __global__ void __launch_bounds__(256, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, bf16* __restrict__ out, float* __restrict__ lse,
-                       int T, int H, float scale_log2) {
+                       int T, int H, float scale_log2, unsigned long long* __restrict__ trace) {
   using C = TcFwdCfg<D>;
+  // optional phase timeline of CTA (0, 0) (ZPP_ATTN_TRACE; trace == nullptr in production)
+  const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+  auto mark = [&](int slot) {
+    if (tr) trace[slot] = clock64();
+  };
   constexpr int NA = D / 64;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -133,9 +138,13 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(q_full, 0);
       issue_s(0);
       for (int i = 0; i < nkb; ++i) {
+        mark(16 * i + 0);
         if (i + 1 < nkb) issue_s(i + 1);
+        mark(16 * i + 1);
         mbar_wait(p_full, i & 1);
+        mark(16 * i + 2);
         mbar_wait(v_full0 + 8 * (i & 1), (i >> 1) & 1);
+        mark(16 * i + 3);
         tc_fence_after();
         const uint32_t vb = base + C::V_OFF + (i & 1) * C::TILE;
 #pragma unroll
@@ -154,8 +163,11 @@ __global__ void __launch_bounds__(256, 1)
     const int r = q * 32 + lane;  // query row within the block == TMEM lane
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
     float m_run = -INFINITY, l = 0.f;
+    const bool tl0 = threadIdx.x == 128;
     for (int i = 0; i < nkb; ++i) {
+      if (tl0) mark(16 * i + 8);
       mbar_wait(s_full0 + 8 * (i & 1), (i >> 1) & 1);
+      if (tl0) mark(16 * i + 9);
       tc_fence_after();
       float x[128];  // raw scores (scale folded into the exp2 FFMA below)
       {
@@ -198,8 +210,10 @@ __global__ void __launch_bounds__(256, 1)
         ps[j & 7] += x[j];
       }
       const float rs = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+      if (tl0) mark(16 * i + 10);
       if (i > 0) {
         mbar_wait(o_done, (i - 1) & 1);  // PV_{i-1} finished: P buffer free, O stable
+        if (tl0) mark(16 * i + 11);
         tc_fence_after();
         if (rescale) {
           const float f = fast_exp2(m_run - m_use);
@@ -232,6 +246,7 @@ __global__ void __launch_bounds__(256, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(p_full);
+      if (tl0) mark(16 * i + 12);
     }
     mbar_wait(o_done, (nkb - 1) & 1);
     tc_fence_after();
@@ -276,7 +291,28 @@ int attn_fwd_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int
     set = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  attn_fwd_tc_kernel<D><<<dim3(T / 128, B * H), 256, C::SMEM, s>>>(m, (bf16*)out, lse, T, H, scale_log2);
+  static int want_trace = -1;
+  if (want_trace < 0) want_trace = getenv("ZPP_ATTN_TRACE") ? 1 : 0;
+  unsigned long long* trace = nullptr;
+  if (want_trace) {
+    cudaMalloc(&trace, 16 * 32 * sizeof(unsigned long long));
+    cudaMemset(trace, 0, 16 * 32 * sizeof(unsigned long long));
+  }
+  attn_fwd_tc_kernel<D><<<dim3(T / 128, B * H), 256, C::SMEM, s>>>(m, (bf16*)out, lse, T, H, scale_log2, trace);
+  if (trace) {
+    unsigned long long hbuf[16 * 32];
+    cudaMemcpy(hbuf, trace, sizeof(hbuf), cudaMemcpyDeviceToHost);
+    const int nkb = T / 128;
+    const unsigned long long t0 = hbuf[0];
+    for (int i = 0; i < nkb; ++i) {
+      const unsigned long long* x = hbuf + 16 * i;
+      printf("fwd it %2d | mma: top %7lld s_next %7lld pfull %7lld vfull %7lld | sm: top %7lld sfull %7lld exp %7lld"
+             " odone %7lld parrive %7lld\n", i, (long long)(x[0] - t0), (long long)(x[1] - t0), (long long)(x[2] - t0),
+             (long long)(x[3] - t0), (long long)(x[8] - t0), (long long)(x[9] - t0), (long long)(x[10] - t0),
+             (long long)(i ? x[11] - t0 : 0), (long long)(x[12] - t0));
+    }
+    cudaFree(trace);
+  }
   return check_launch("attn_fwd_tc");
 }
 
@@ -294,8 +330,10 @@ template int attn_fwd_tc_launch<128>(const void*, void*, float*, int, int, int, 
 //                   dQ  = dS K_j    (A = dS^T smem read MN-major)  (TMEM cols 384.., over dP^T)
 //   warps 4-7  thread t owns key row t: P^T = exp2(S^T*scale*log2e - lse*log2e) (causal mask
 //              on the diagonal block), dS^T = P^T (dP^T - delta) * scale; P^T -> TMEM
-//              (over S^T), dS^T -> smem.  Then dQ rows (thread = query row) are staged in the
-//              (now free) dS^T smem and TMA reduce-added into the fp32 dQ workspace.
+//              (over S^T), dS^T -> smem.  Then dQ rows (thread = query row) are read from
+//              TMEM into registers and the dP columns released at once (the next dP^T
+//              does not wait for the reduction), then staged in the free dS^T smem and
+//              TMA reduce-added into the fp32 dQ workspace.
 // smem (d=128): K 32 KB, V 32 KB, Q/dO 2 x 64 KB, dS^T 32 KB (+ lse/delta 1 KB).
 template <int D>
 struct TcBwdCfg {
@@ -316,8 +354,8 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
-                       const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, float scale,
-                       unsigned long long* __restrict__ trace) {
+                       const float* __restrict__ delta, bf16* __restrict__ dqkv, float* __restrict__ dq_acc,
+                       int T, int H, float scale, unsigned long long* __restrict__ trace) {
   using C = TcBwdCfg<D>;
   // optional phase timeline of CTA (0, 0) for performance analysis (trace == nullptr in production)
   const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
@@ -518,14 +556,20 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int cc = 0; cc < NCH; ++cc) tmem_ld32(T_DP + lo + (hh * NCH + cc) * 32, dqv[cc]);
       tmem_wait_ld();
-      const uint32_t ebuf = base + C::DS_OFF + (warp - 4) * 4096;
+      tc_fence_before();
+      mbar_arrive(dq_free);  // dQ is in registers: the dP columns may receive the next dP^T now
+      if (r == 0 && hh == 0) mark(16 * it + 13);
+      // stage each 32x32 fp32 chunk in this warp's 4 KB slice of the (free) dS^T tile and
+      // TMA reduce-add it into the dQ workspace; runs while the next dP^T computes
+      const uint32_t buf = base + C::DS_OFF + (warp - 4) * 4096;
 #pragma unroll
       for (int cc = 0; cc < NCH; ++cc) {
         const int c = hh * NCH + cc;
-        uint32_t (&v)[32] = dqv[cc];
-        const uint32_t buf = ebuf;
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
+        const uint32_t* v = dqv[cc];
+        if (cc > 0) {
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           st_shared_v4(buf + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -535,12 +579,8 @@ __global__ void __launch_bounds__(384, 1)
           tma_reduce_add_2d(&tm_dq, buf, h * D + c * 32, row_base + q0 + q * 32);
           bulk_commit();
         }
-
       }
-      tc_fence_before();
-      mbar_arrive(dq_free);  // the dP columns may now receive the next dP^T
-      if (r == 0 && hh == 0) mark(16 * it + 13);
-      if (lane == 0) bulk_wait_read<0>();  // staging lives in the dS^T tile the next iteration rewrites
+      if (lane == 0) bulk_wait_read<0>();  // the staging slice is rewritten as dS^T next iteration
       __syncwarp();
       if (r == 0 && hh == 0) mark(16 * it + 14);
     }
@@ -614,8 +654,8 @@ int attn_bwd_tc_launch(const void* qkv, const void* dout, const float* lse, cons
   if (want_trace < 0) want_trace = getenv("ZPP_ATTN_TRACE") ? 1 : 0;
   unsigned long long* trace = nullptr;
   if (want_trace) cudaMalloc(&trace, 16 * 32 * sizeof(unsigned long long));
-  attn_bwd_tc_kernel<D><<<dim3(T / 128, B * H), 384, C::SMEM, s>>>(mq, mdo, mdq, lse, delta, (bf16*)dqkv, T, H,
-                                                                    1.f / sqrtf((float)D), trace);
+  attn_bwd_tc_kernel<D><<<dim3(T / 128, B * H), 384, C::SMEM, s>>>(mq, mdo, mdq, lse, delta, (bf16*)dqkv, dq_acc,
+                                                                    T, H, 1.f / sqrtf((float)D), trace);
   if (trace) {
     unsigned long long h[16 * 32];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);

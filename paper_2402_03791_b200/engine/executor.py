@@ -115,7 +115,8 @@ class _Stage:
         self.sub, self.nsub = sub, nsub
         self.gathered = torch.zeros(n, dtype=BF16, device=dev)
         self.shard_bf16 = self.gathered[z * ns:(z + 1) * ns]      # in-place all-gather layout
-        self.sub_bf16 = self.shard_bf16[node * nsub:(node + 1) * nsub]  # AG_PARAM_INTER layout
+        sub_i = node if sub > 1 else 0  # DP outer mode: every replica updates its whole shard
+        self.sub_bf16 = self.shard_bf16[sub_i * nsub:(sub_i + 1) * nsub]  # AG_PARAM_INTER layout
         self.master = torch.zeros(nsub, dtype=F32, device=dev)
         self.exp_avg = torch.zeros(nsub, dtype=F32, device=dev)
         self.exp_avg_sq = torch.zeros(nsub, dtype=F32, device=dev)

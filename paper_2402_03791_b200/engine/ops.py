@@ -217,16 +217,23 @@ def xent(logits, labels, loss_sum, grad_scale, stream=None):
 
 
 def cast_scale(src_f32, dst_bf16, scale=1.0, stream=None):
+    if src_f32.numel() != dst_bf16.numel():
+        raise ValueError("cast_scale: size mismatch")
     _count(1)
     lib.call("zpp_cast_scale_f32_bf16", _p(src_f32), _p(dst_bf16), src_f32.numel(), scale, _s(stream))
 
 
 def accum(src_bf16, acc_f32, stream=None):
+    if src_bf16.numel() != acc_f32.numel():
+        raise ValueError("accum: size mismatch")
     _count(1)
     lib.call("zpp_accum_bf16_f32", _p(src_bf16), _p(acc_f32), src_bf16.numel(), _s(stream))
 
 
 def adamw(master, m, v, grad, param_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
+    n = master.numel()
+    if not (m.numel() == v.numel() == grad.numel() == param_bf16.numel() == n):
+        raise ValueError("adamw: master / exp_avg / exp_avg_sq / grad / bf16 param sizes differ")
     _count(1)
     lib.call("zpp_adamw", _p(master), _p(m), _p(v), _p(grad), _p(param_bf16), master.numel(), lr, beta1,
              beta2, eps, wd, step, _s(stream))

@@ -27,4 +27,15 @@ for name,M,N,K,at,bt,ep in shapes:
             ts.append(s.elapsed_time(t))
         ts.sort(); ms = ts[len(ts)//2]
         res.append((ms, 2*M*N*K/ms/1e9))
-    print(f"{name:11s} {M}x{N}x{K}: nosk {res[0][0]*1e3:8.1f} us {res[0][1]:7.1f} TF/s | sk {res[1][0]*1e3:8.1f} us {res[1][1]:7.1f} TF/s  ({res[0][0]/res[1][0]:.3f}x)", flush=True)
+    # cuBLAS reference for the same shape (bf16 out; timing comparison only)
+    Ab = A.t() if at else A
+    Bb = B if bt else B.t()
+    for _ in range(3): torch.matmul(Ab, Bb)
+    ts = []
+    for _ in range(10):
+        flush.zero_()
+        s, t = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record(); torch.matmul(Ab, Bb); t.record(); torch.cuda.synchronize()
+        ts.append(s.elapsed_time(t))
+    ts.sort(); cub = ts[len(ts)//2]
+    print(f"{name:11s} {M}x{N}x{K}: cublas {cub*1e3:8.1f} us {2*M*N*K/cub/1e9:7.1f} TF/s | nosk {res[0][0]*1e3:8.1f} us {res[0][1]:7.1f} TF/s | sk {res[1][0]*1e3:8.1f} us {res[1][1]:7.1f} TF/s  ({res[0][0]/res[1][0]:.3f}x)", flush=True)
