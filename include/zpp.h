@@ -86,6 +86,11 @@ int zpp_layernorm_bwd(const void* dy, const void* x, const float* mean, const fl
                       const void* dresid, void* dx, float* dgamma, float* dbeta, float* workspace, int rows,
                       int cols, int accumulate, uintptr_t stream);
 long long zpp_layernorm_bwd_workspace_floats(int rows, int cols);
+/* The parameter-gradient half of zpp_layernorm_bwd / zpp_rmsnorm_bwd on its own (those skip it when
+ * dgamma == NULL), so it can run on a side stream: dgamma (+)= sum_r dy*xhat, dbeta (+)= sum_r dy
+ * (dbeta may be NULL; mean == NULL means RMSNorm, xhat = x*rstd). */
+int zpp_norm_param_grads(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma,
+                         float* dbeta, float* workspace, int rows, int cols, int accumulate, uintptr_t stream);
 
 /* ---- LLaMA block pieces: RMSNorm, SwiGLU, rotary embedding ----------------------- */
 /* y = x * rstd * gamma, rstd = 1/sqrt(mean(x^2) + eps) (fp32 rstd out, [rows]) */

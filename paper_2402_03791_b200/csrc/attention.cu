@@ -27,6 +27,9 @@ typedef __nv_bfloat16 bf16;
 template <int D>
 int attn_fwd_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s);
 template <int D>
+int attn_bwd_split_tc_launch(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
+                             int B, int T, int H, cudaStream_t s);
+template <int D>
 int attn_bwd_tc_launch(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
                        float* dq_acc, int B, int T, int H, cudaStream_t s);
 
@@ -253,6 +256,7 @@ __global__ void attn_delta_kernel(const bf16* __restrict__ out, const bf16* __re
 #pragma unroll
   for (int x = 16; x > 0; x >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, x);
   if (lane == 0) delta[((long long)b * H + h) * T + t] = acc;
+  if (!dq) return;
   float4* z = reinterpret_cast<float4*>(dq + w * D);
   for (int i = lane; i < D / 4; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
@@ -458,6 +462,14 @@ static int attn_fwd_launch(const void* qkv, void* out, float* lse, int B, int T,
   return check_launch("attn_fwd");
 }
 
+// Two-kernel tcgen05 backward (attention_bwd_tc.cu) unless ZPP_ATTN_BWD_FUSED=1 selects the
+// fused key-outer kernel with fp32 dQ reduction (kept for comparison).
+static bool bwd_split() {
+  static int v = -1;
+  if (v < 0) v = getenv("ZPP_ATTN_BWD_FUSED") ? 0 : 1;
+  return v == 1;
+}
+
 template <int D>
 static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, const void* dout, void* dqkv,
                            float* ws, int B, int T, int H, cudaStream_t s, bool use_tc) {
@@ -472,10 +484,12 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
   float* dq = ws + (long long)B * H * T;
   const long long nrows = (long long)B * T;
   const long long warps = nrows * H;
-  attn_delta_kernel<D><<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>((const bf16*)out, (const bf16*)dout, delta, dq,
-                                                                      B, T, H);
+  const bool split = use_tc && bwd_split();
+  attn_delta_kernel<D><<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>((const bf16*)out, (const bf16*)dout, delta,
+                                                                      split ? nullptr : dq, B, T, H);
   int rc = check_launch("attn_delta");
   if (rc) return rc;
+  if (split) return attn_bwd_split_tc_launch<D>(qkv, dout, lse, delta, dqkv, B, T, H, s);
   if (use_tc) {
     rc = attn_bwd_tc_launch<D>(qkv, dout, lse, delta, dqkv, dq, B, T, H, s);
   } else {
@@ -499,6 +513,7 @@ using namespace zpp;
 
 namespace zpp {
 int attention_tc_preload();
+int attention_bwd_tc_preload();
 int gemm_preload();
 int kernels_preload();
 }  // namespace zpp
@@ -510,6 +525,8 @@ extern "C" int zpp_preload_kernels(void) {
   int rc = gemm_preload();
   if (rc) return rc;
   rc = attention_tc_preload();
+  if (rc) return rc;
+  rc = attention_bwd_tc_preload();
   if (rc) return rc;
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, attn_fwd_kernel<64>);

@@ -565,12 +565,12 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
                                  const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
                                  float* workspace, int rows, int cols, int accumulate, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
-  if (!workspace) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
+  if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
   layernorm_bwd_dx_kernel<false><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
                                                              (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
-  if (rc) return rc;
+  if (rc || !dgamma) return rc;  // dgamma == null: parameter grads via zpp_norm_param_grads
   return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, accumulate,
                        STREAM(stream));
 }
@@ -588,14 +588,24 @@ extern "C" int zpp_rmsnorm_bwd(const void* dy, const void* x, const float* rstd,
                                const void* dresid, void* dx, float* dgamma, float* workspace, int rows, int cols,
                                int accumulate, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: cols % 8 != 0 or > 8192");
-  if (!workspace) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: workspace required");
+  if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
   layernorm_bwd_dx_kernel<true><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, nullptr, rstd,
                                                                   (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx,
                                                                   cols);
   int rc = check_launch("rmsnorm_bwd_dx");
-  if (rc) return rc;
+  if (rc || !dgamma) return rc;
   return colred_launch(true, dy, cols, x, nullptr, rstd, dgamma, nullptr, workspace, rows, cols, accumulate,
+                       STREAM(stream));
+}
+
+extern "C" int zpp_norm_param_grads(const void* dy, const void* x, const float* mean, const float* rstd,
+                                    float* dgamma, float* dbeta, float* workspace, int rows, int cols, int accumulate,
+                                    uintptr_t stream) {
+  if (cols % 8) return set_error(ZPP_ERR_ARG, "norm_param_grads: cols % 8 != 0");
+  if (!workspace || !dgamma) return set_error(ZPP_ERR_ARG, "norm_param_grads: workspace and dgamma required");
+  if (rows <= 0) return ZPP_OK;
+  return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, accumulate,
                        STREAM(stream));
 }
 

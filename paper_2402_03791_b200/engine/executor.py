@@ -192,6 +192,9 @@ class Runtime:
         mk = lambda: torch.cuda.Stream(device=self.dev)  # noqa: E731
         self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
         self.s_act_send, self.s_act_recv, self.s_grad_send, self.s_grad_recv = mk(), mk(), mk(), mk()
+        # parameter-gradient column reductions (bias, norm gamma / beta) only feed RS / OPT:
+        # they run on this side stream beside the next GEMMs (ZPP_AUX_STREAM=0 keeps them inline)
+        self.s_aux = mk() if os.environ.get("ZPP_AUX_STREAM", "1") != "0" else self.s_comp
         T, h = spec.tokens_per_microbatch, spec.hidden
         # column-reduction workspaces carry re-armed tickets: zero them once
         self.ln_ws = torch.zeros(ops.layernorm_bwd_workspace(T, h), dtype=F32, device=self.dev)
@@ -384,6 +387,7 @@ class Runtime:
             return  # the stage grad IS the shard grad; nothing moves (0 bytes)
         rs = self.s_rs
         rs.wait_event(self._record(self.s_comp))   # all B/W of (s, u) enqueued before this point
+        self._join_aux(rs)                           # ... and their parameter-grad reductions
         self._begin(rs)
         n, ns = st.lay.numel, st.lay.shard_numel
         send, recv = self.rs_send[:n], self.rs_recv[:ns]
@@ -405,6 +409,7 @@ class Runtime:
             return  # 0-byte task (ZeRO-1 mode on one node)
         rs = self.s_rs
         rs.wait_event(self._record(self.s_comp))  # D == 1: W wrote grad_shard on compute
+        self._join_aux(rs)
         self._begin(rs)
         comm = self.comms[("inter",)]
         for st in self.stages.values():
@@ -442,6 +447,7 @@ class Runtime:
     def _optimizer(self) -> None:
         for ev in self._rs_events:
             self._wait(ev, "zero")
+        self._join_aux(self.s_comp)  # D == 1: bias / norm grads reduced on aux feed this update
         spec = self.spec
         for st in self.stages.values():
             ops.adamw(st.master, st.exp_avg, st.exp_avg_sq, st.grad_sub, st.sub_bf16, spec.lr, spec.beta1,
@@ -557,6 +563,34 @@ class Runtime:
             x = x2
         return layers, x
 
+    def _aux(self, *hold: torch.Tensor):
+        """The side stream, ordered after everything enqueued on compute so far; ``hold``
+        tensors are kept alive for it (caching-allocator stream tracking)."""
+        if self.s_aux is self.s_comp:
+            return self.s_comp
+        self.s_aux.wait_event(self._record(self.s_comp))
+        for t in hold:
+            t.record_stream(self.s_aux)
+        return self.s_aux
+
+    def _join_aux(self, stream) -> None:
+        if self.s_aux is not self.s_comp:
+            stream.wait_event(self._record(self.s_aux))
+
+    def _norm_bwd(self, st: "_Stage", dy, x, mean, rstd, gkey, bkey, dx, dresid=None) -> None:
+        """LayerNorm (mean given) / RMSNorm backward: dx on compute, gamma / beta grads on aux."""
+        P, G = st.p, st.g
+        if mean is None:
+            ops.rmsnorm_bwd(dy, x, rstd, P[gkey], dx, None, None, dresid=dresid)
+        else:
+            ops.layernorm_bwd(dy, x, mean, rstd, P[gkey], dx, None, None, None, dresid=dresid)
+        acc = st.accumulate(gkey)
+        if bkey is not None:
+            acc = acc | st.accumulate(bkey)
+        held = (dy, x, rstd) if mean is None else (dy, x, mean, rstd)
+        ops.norm_param_grads(dy, x, mean, rstd, G[gkey], G[bkey] if bkey is not None else None, self.ln_ws,
+                             accumulate=acc, stream=self._aux(*held))
+
     def _final_norm(self, st: "_Stage", out: torch.Tensor):
         spec, P = self.spec, st.p
         T, h = out.shape
@@ -569,15 +603,10 @@ class Runtime:
         return xf, {"xlast": out, "muf": muf, "rf": rf}
 
     def _final_norm_bwd(self, st: "_Stage", stash: dict, dxf: torch.Tensor) -> torch.Tensor:
-        P, G = st.p, st.g
         dx = torch.empty_like(dxf)
-        if self.spec.llama:
-            ops.rmsnorm_bwd(dxf, stash.pop("xlast"), stash.pop("rf"), P[("lnf_g", None)], dx, G[("lnf_g", None)],
-                            self.ln_ws, accumulate=st.accumulate(("lnf_g", None)))
-            return dx
-        ops.layernorm_bwd(dxf, stash.pop("xlast"), stash.pop("muf"), stash.pop("rf"), P[("lnf_g", None)], dx,
-                          G[("lnf_g", None)], G[("lnf_b", None)], self.ln_ws,
-                          accumulate=st.accumulate(("lnf_g", None)) | st.accumulate(("lnf_b", None)))
+        llama = self.spec.llama
+        self._norm_bwd(st, dxf, stash.pop("xlast"), None if llama else stash.pop("muf"), stash.pop("rf"),
+                       ("lnf_g", None), None if llama else ("lnf_b", None), dx)
         return dx
 
     def _forward(self, s: int, m: int) -> None:
@@ -650,9 +679,7 @@ class Runtime:
             dxn2 = e(T, h)
             ops.gemm(du, P[("w_fc1", l)], dxn2, b_t=True)
             dx1 = e(T, h)
-            ops.layernorm_bwd(dxn2, a["x1"], a["mu2"], a["r2"], P[("ln2_g", l)], dx1, G[("ln2_g", l)],
-                              G[("ln2_b", l)], self.ln_ws, dresid=d2,
-                              accumulate=st.accumulate(("ln2_g", l)) | st.accumulate(("ln2_b", l)))
+            self._norm_bwd(st, dxn2, a["x1"], a["mu2"], a["r2"], ("ln2_g", l), ("ln2_b", l), dx1, dresid=d2)
             do = e(T, h)
             ops.gemm(dx1, P[("w_proj", l)], do, b_t=True)
             dqkv = e(T, 3 * h)
@@ -660,9 +687,7 @@ class Runtime:
             dxn1 = e(T, h)
             ops.gemm(dqkv, P[("w_qkv", l)], dxn1, b_t=True)
             dxl = e(T, h)
-            ops.layernorm_bwd(dxn1, a["x"], a["mu1"], a["r1"], P[("ln1_g", l)], dxl, G[("ln1_g", l)],
-                              G[("ln1_b", l)], self.ln_ws, dresid=dx1,
-                              accumulate=st.accumulate(("ln1_g", l)) | st.accumulate(("ln1_b", l)))
+            self._norm_bwd(st, dxn1, a["x"], a["mu1"], a["r1"], ("ln1_g", l), ("ln1_b", l), dxl, dresid=dx1)
             # keep only what W needs: inputs of the linears and their output grads
             stash["layers"][i] = {"xn1": a["xn1"], "o": a["o"], "xn2": a["xn2"], "g": a["g"],
                                   "d2": d2, "du": du, "dx1": dx1, "dqkv": dqkv}
@@ -690,8 +715,7 @@ class Runtime:
         dxn2 = e(T, h)
         ops.gemm(dgu, P[("w_fc1", l)], dxn2, b_t=True)
         dx1 = e(T, h)
-        ops.rmsnorm_bwd(dxn2, a["x1"], a["r2"], P[("ln2_g", l)], dx1, G[("ln2_g", l)], self.ln_ws, dresid=d2,
-                        accumulate=st.accumulate(("ln2_g", l)))
+        self._norm_bwd(st, dxn2, a["x1"], None, a["r2"], ("ln2_g", l), None, dx1, dresid=d2)
         do = e(T, h)
         ops.gemm(dx1, P[("w_proj", l)], do, b_t=True)
         dqkv = e(T, 3 * h)
@@ -700,8 +724,7 @@ class Runtime:
         dxn1 = e(T, h)
         ops.gemm(dqkv, P[("w_qkv", l)], dxn1, b_t=True)
         dxl = e(T, h)
-        ops.rmsnorm_bwd(dxn1, a["x"], a["r1"], P[("ln1_g", l)], dxl, G[("ln1_g", l)], self.ln_ws, dresid=dx1,
-                        accumulate=st.accumulate(("ln1_g", l)))
+        self._norm_bwd(st, dxn1, a["x"], None, a["r1"], ("ln1_g", l), None, dxl, dresid=dx1)
         layers[i] = {"xn1": a["xn1"], "o": a["o"], "xn2": a["xn2"], "a": a["a"],
                      "d2": d2, "dgu": dgu, "dx1": dx1, "dqkv": dqkv}
         return dxl
@@ -716,13 +739,17 @@ class Runtime:
                     ("dqkv", "xn1", "w_qkv", None)) if self.spec.llama else
                    (("d2", "g", "w_fc2", "b_fc2"), ("du", "xn2", "w_fc1", "b_fc1"),
                     ("dx1", "o", "w_proj", "b_proj"), ("dqkv", "xn1", "w_qkv", "b_qkv")))
+        if not self.spec.llama:  # bias grads: column sums of the linears' output grads, on aux
+            aux = self._aux(*[stash["layers"][i][dy] for i in range(hi - lo) for dy, _, _, _ in linears])
+            for i, l in enumerate(range(lo, hi)):
+                a = stash["layers"][i]
+                for dy, _, _, bias in linears:
+                    ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws, accumulate=st.accumulate((bias, l)), stream=aux)
         for i, l in enumerate(range(lo, hi)):
             a = stash["layers"][i]
             for dy, x, w, bias in linears:
                 ops.gemm(a[dy], a[x], G[(w, l)], a_t=True, b_t=True,
                          epilogue=ops.EPI_F32_ACC if st.accumulate((w, l)) else ops.EPI_F32)
-                if bias is not None:
-                    ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws, accumulate=st.accumulate((bias, l)))
         if s == self.S - 1:
             ops.gemm(stash["dlogits"], stash["xf"], G[("w_lm", None)], a_t=True, b_t=True,
                      epilogue=ops.EPI_F32_ACC if st.accumulate(("w_lm", None)) else ops.EPI_F32)

@@ -121,9 +121,18 @@ def layernorm_bwd(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, workspace, dresid
                   stream=None):
     """dgamma/dbeta += column sums, or = when ``accumulate`` is False (first writer)."""
     rows, cols = x.shape
-    _count(2)
+    _count(1 if dgamma is None else 2)
     lib.call("zpp_layernorm_bwd", _p(dy), _p(x), _p(mean), _p(rstd), _p(gamma), _p(dresid), _p(dx),
              _p(dgamma), _p(dbeta), _p(workspace), rows, cols, int(accumulate), _s(stream))
+
+
+def norm_param_grads(dy, x, mean, rstd, dgamma, dbeta, workspace, accumulate=True, stream=None):
+    """LayerNorm (mean given) / RMSNorm (mean None) gamma / beta grads alone; pairs with
+    layernorm_bwd / rmsnorm_bwd called with dgamma=None."""
+    rows, cols = x.shape
+    _count(1)
+    lib.call("zpp_norm_param_grads", _p(dy), _p(x), _p(mean), _p(rstd), _p(dgamma), _p(dbeta), _p(workspace),
+             rows, cols, int(accumulate), _s(stream))
 
 
 def rmsnorm_fwd(x, gamma, y, rstd, eps=1e-5, stream=None):
@@ -135,7 +144,7 @@ def rmsnorm_fwd(x, gamma, y, rstd, eps=1e-5, stream=None):
 def rmsnorm_bwd(dy, x, rstd, gamma, dx, dgamma, workspace, dresid=None, accumulate=True, stream=None):
     """dgamma += column sums of dy * xhat, or = when ``accumulate`` is False (first writer)."""
     rows, cols = x.shape
-    _count(2)
+    _count(1 if dgamma is None else 2)
     lib.call("zpp_rmsnorm_bwd", _p(dy), _p(x), _p(rstd), _p(gamma), _p(dresid), _p(dx), _p(dgamma),
              _p(workspace), rows, cols, int(accumulate), _s(stream))
 
