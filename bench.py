@@ -114,7 +114,7 @@ class Clocks:
             return None
         self.proc.terminate()
         self.proc.wait()
-        sm, mx, reasons = [], 0.0, set()
+        sm, pw, mx, reasons = [], [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
@@ -123,6 +123,7 @@ class Clocks:
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for n, v in zip(names, f[5:9]):
@@ -131,7 +132,8 @@ class Clocks:
         if not sm:
             return None
         loaded = [x for x in sm if x > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons)}
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # --------------------------------------------------------------------------- GPU leg

@@ -27,6 +27,8 @@ typedef __nv_bfloat16 bf16;
 template <int D>
 int attn_fwd_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s);
 template <int D>
+int attn_fwd2_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s);
+template <int D>
 int attn_bwd_split_tc_launch(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
                              int B, int T, int H, cudaStream_t s);
 template <int D>
@@ -513,6 +515,7 @@ using namespace zpp;
 
 namespace zpp {
 int attention_tc_preload();
+int attention_fwd2_preload();
 int attention_bwd_tc_preload();
 int gemm_preload();
 int kernels_preload();
@@ -528,6 +531,8 @@ extern "C" int zpp_preload_kernels(void) {
   if (rc) return rc;
   rc = attention_bwd_tc_preload();
   if (rc) return rc;
+  rc = attention_fwd2_preload();
+  if (rc) return rc;
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, attn_fwd_kernel<64>);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, attn_fwd_kernel<128>);
@@ -541,10 +546,12 @@ extern "C" int zpp_preload_kernels(void) {
   return kernels_preload();
 }
 
-static int g_attn_impl = 0;  // 0 = auto (tcgen05 when seq % 128 == 0), 1 = mma.sync FA2 tiles
+// 0 = auto (tcgen05; two query tiles per CTA when seq % 256 == 0), 1 = mma.sync FA2 tiles,
+// 2 = tcgen05 with one query tile per CTA (forward only; comparison / tests)
+static int g_attn_impl = 0;
 
 extern "C" int zpp_attn_set_impl(int impl) {
-  if (impl < 0 || impl > 1) return set_error(ZPP_ERR_ARG, "attn impl must be 0 or 1");
+  if (impl < 0 || impl > 2) return set_error(ZPP_ERR_ARG, "attn impl must be 0, 1 or 2");
   g_attn_impl = impl;
   return ZPP_OK;
 }
@@ -553,7 +560,11 @@ extern "C" int zpp_attn_fwd(const void* qkv, void* out, float* lse, int batch, i
                             uintptr_t stream) {
   if (seq % 64) return set_error(ZPP_ERR_ARG, "attn: seq must be a multiple of 64");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (g_attn_impl == 0 && seq % 128 == 0) {
+  if (g_attn_impl == 0 && seq % 256 == 0) {
+    if (head_dim == 128) return attn_fwd2_tc_launch<128>(qkv, out, lse, batch, seq, heads, s);
+    if (head_dim == 64) return attn_fwd2_tc_launch<64>(qkv, out, lse, batch, seq, heads, s);
+  }
+  if (g_attn_impl != 1 && seq % 128 == 0) {
     if (head_dim == 128) return attn_fwd_tc_launch<128>(qkv, out, lse, batch, seq, heads, s);
     if (head_dim == 64) return attn_fwd_tc_launch<64>(qkv, out, lse, batch, seq, heads, s);
   }
@@ -570,7 +581,7 @@ extern "C" int zpp_attn_bwd(const void* qkv, const void* out, const float* lse, 
                             float* workspace, int batch, int seq, int heads, int head_dim, uintptr_t stream) {
   if (seq % 64) return set_error(ZPP_ERR_ARG, "attn_bwd: seq must be a multiple of 64");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const bool tc = g_attn_impl == 0 && seq % 128 == 0;
+  const bool tc = g_attn_impl != 1 && seq % 128 == 0;
   if (head_dim == 128) return attn_bwd_launch<128>(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, s, tc);
   if (head_dim == 64) return attn_bwd_launch<64>(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, s, tc);
   return set_error(ZPP_ERR_ARG, "attn_bwd: head_dim must be 64 or 128");

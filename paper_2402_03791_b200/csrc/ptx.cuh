@@ -264,6 +264,16 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (offloads the MUFU unit, which bounds softmax phases): round-to-nearest
+// split x = j + f with the 1.5*2^23 trick, degree-3 minimax 2^f on [-0.5, 0.5] (relative error
+// 1.0e-4, far below bf16 rounding), exponent added as an integer.  exp2_poly(-inf) == 0.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221098f), f, 0.69328293f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 }  // namespace zpp
 
 namespace zpp {

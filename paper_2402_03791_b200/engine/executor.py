@@ -87,6 +87,7 @@ class StepResult:
     task_times: dict = field(default_factory=dict)
     exposed_comm_ms: float | None = None    # compute-stream waits on AG / RS
     p2p_wait_ms: float | None = None        # compute-stream waits on P2P recv (bubble + transfer)
+    waits: list | None = None               # (kind, task_id, ms) of every timed compute-stream wait
     busy_ms: float | None = None
     sim: object = None                      # timeline runtimes: the whole-job SimResult (engine.timeline)
 
@@ -100,6 +101,23 @@ class StepResult:
             if name in sim.extras:
                 return sim.extras[name]
         raise AttributeError(name)
+
+
+def opt_chunks(lay: StageLayout) -> dict:
+    """Partition of the flat stage buffer [0, numel) into optimizer chunks: "embed"
+    (wte, wpe), one per layer, and "head" (final norm + LM head); alignment padding goes
+    with the preceding tensor.  AdamW is elementwise, so updating chunk by chunk is
+    bit-identical to one launch over the whole buffer."""
+    keys = []
+    for sl in lay.slots:
+        keys.append("embed" if sl.name in ("wte", "wpe") else
+                    "head" if sl.layer is None else sl.layer)
+    out: dict = {}
+    for i, (sl, k) in enumerate(zip(lay.slots, keys)):
+        end = lay.slots[i + 1].offset if i + 1 < len(lay.slots) else lay.numel
+        lo, hi = out.get(k, (sl.offset, end))
+        out[k] = (min(lo, sl.offset), max(hi, end))
+    return out
 
 
 class _Stage:
@@ -130,12 +148,18 @@ class _Stage:
             self.p[key] = self.gathered[s.offset:s.offset + s.numel].view(*s.shape)
             self.g[key] = self.grad_full[s.offset:s.offset + s.numel].view(*s.shape)
         self.ag_event = None        # compute must wait before using gathered params
+        self.opt_ready = None       # this stage's shard is updated (early optimizer); AG waits here
         self.grad_free_event = None  # compute must wait before writing grad_full again
         # Gradients are never memset: the first writer of each tensor in an accumulation
         # window (a step at D == 1, one unit's reduce-scatter at D > 1) stores instead of
         # accumulating.  Only the embedding grads (row scatter-add) are zeroed.
         self.scatter_keys = [k for k in self.g if k[0] in ("wte", "wpe")]
         self.new_window()
+        self.chunks = opt_chunks(lay)
+
+    def opt_slice(self, key):
+        """(lo, hi) element range of optimizer chunk ``key`` ("embed", "head" or a layer)."""
+        return self.chunks[key]
 
     def new_window(self) -> None:
         self.fresh = set(self.g).difference(self.scatter_keys)
@@ -195,6 +219,18 @@ class Runtime:
         # parameter-gradient column reductions (bias, norm gamma / beta) only feed RS / OPT:
         # they run on this side stream beside the next GEMMs (ZPP_AUX_STREAM=0 keeps them inline)
         self.s_aux = mk() if os.environ.get("ZPP_AUX_STREAM", "1") != "0" else self.s_comp
+        # Early optimizer: a stage's AdamW starts on its own stream as soon as the stage's
+        # gradients are final (its last W at D == 1, layer by layer; its last RS_GRAD at
+        # D > 1), overlapping the remaining B / W work instead of trailing the step.  The OPT
+        # task still orders everything after it (ZPP_EARLY_OPT=0: OPT runs it all, as before).
+        self.early_opt = self.n == 1 and os.environ.get("ZPP_EARLY_OPT", "1") != "0"
+        self.s_opt = mk()
+        self._final_w, self._final_rs = {}, {}
+        for i, t in enumerate(self.tasks):
+            if t.kind is TaskKind.W:
+                self._final_w[t.stage] = i
+            elif t.kind is TaskKind.RS_GRAD:
+                self._final_rs[t.stage] = i
         T, h = spec.tokens_per_microbatch, spec.hidden
         # column-reduction workspaces carry re-armed tickets: zero them once
         self.ln_ws = torch.zeros(ops.layernorm_bwd_workspace(T, h), dtype=F32, device=self.dev)
@@ -270,7 +306,7 @@ class Runtime:
             e0 = self._record(self.s_comp, True)
             self.s_comp.wait_event(ev)
             e1 = self._record(self.s_comp, True)
-            self._waits.append((kind, e0, e1))
+            self._waits.append((kind, e0, e1, self.tasks[self._ti].task_id))
             self._task_start = e1  # the task's own work starts after its last wait
         else:
             self.s_comp.wait_event(ev)
@@ -308,7 +344,10 @@ class Runtime:
         trace = _TRACE and self.step_count <= 2
         with torch.cuda.stream(comp):
             ops.zero(self.loss_sum, stream=comp)
-            for task in self.tasks:
+            self._opt_done: set = set()
+            self._opt_ev = None
+            for ti, task in enumerate(self.tasks):
+                self._ti = ti
                 if trace:
                     print(f"[r{self.rank} {time.perf_counter():.3f}] {task.task_id} "
                           f"alloc={torch.cuda.memory_allocated(self.dev) / 1e9:.1f}G "
@@ -333,8 +372,9 @@ class Runtime:
         if self.timeline:
             res.task_times = {t: (t_start.elapsed_time(a), t_start.elapsed_time(b)) for t, (a, b) in times.items()}
             res.busy_ms = sum(e - s for t, (s, e) in res.task_times.items() if t.is_compute)
-            res.exposed_comm_ms = sum(a.elapsed_time(b) for k, a, b in self._waits if k == "zero")
-            res.p2p_wait_ms = sum(a.elapsed_time(b) for k, a, b in self._waits if k == "p2p")
+            res.waits = [(k, tid, a.elapsed_time(b)) for k, a, b, tid in self._waits]
+            res.exposed_comm_ms = sum(ms for k, _, ms in res.waits if k == "zero")
+            res.p2p_wait_ms = sum(ms for k, _, ms in res.waits if k == "p2p")
         return res
 
     def _stream_of(self, task: Task):
@@ -374,7 +414,9 @@ class Runtime:
         st = self.stages[s]
         if self.D == 1:
             return  # nothing moves; the previous AG_PARAM_INTER's event (if any) stays armed
-        self.s_ag.wait_event(self.opt_event)  # shards are final once the previous OPT ran
+        # shards are final once the previous OPT ran -- for an early-optimized stage, once
+        # its own AdamW ran (the gather then overlaps the previous step's remaining work)
+        self.s_ag.wait_event(st.opt_ready if st.opt_ready is not None else self.opt_event)
         self._begin(self.s_ag)
         ns = st.lay.shard_numel
         lib.call("zpp_allgather", self.comms[("ag", self.p)], st.shard_bf16.data_ptr(),
@@ -398,7 +440,11 @@ class Runtime:
         lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], send.data_ptr(), recv.data_ptr(), ns, 0,
                  rs.cuda_stream)
         ops.accum(recv, st.grad_shard, stream=rs)
-        self._rs_events.append(self._record(rs))
+        ev = self._record(rs)
+        self._rs_events.append(ev)
+        if self.early_opt and self._final_rs.get(s) == self._ti:
+            self._early_opt(st, None, [ev])  # this stage's shard grad is final
+            self._opt_done.add(s)
 
     def _outer_grad(self, reduce_scatter: bool) -> None:
         """AR_GRAD (DP outer, `schedules.py:80-81`) or RS_GRAD_INTER (ZeRO-1 outer,
@@ -444,14 +490,31 @@ class Runtime:
             for st in self.stages.values():
                 st.ag_event = ev       # no AG_PARAM event to wait on: first use waits here
 
+    def _adamw(self, st: _Stage, lo: int, hi: int, stream) -> None:
+        spec = self.spec
+        ops.adamw(st.master[lo:hi], st.exp_avg[lo:hi], st.exp_avg_sq[lo:hi], st.grad_sub[lo:hi],
+                  st.sub_bf16[lo:hi], spec.lr, spec.beta1, spec.beta2, spec.adam_eps, spec.weight_decay,
+                  self.step_count, stream=stream)
+
+    def _early_opt(self, st: _Stage, key, after) -> None:
+        """AdamW of optimizer chunk ``key`` (None = the whole shard) on the opt stream,
+        ordered after the events ``after`` (the chunk's last gradient writers)."""
+        for ev in after:
+            self.s_opt.wait_event(ev)
+        lo, hi = (0, st.nsub) if key is None else st.opt_slice(key)
+        self._adamw(st, lo, hi, self.s_opt)
+        self._opt_ev = st.opt_ready = self._record(self.s_opt)
+
     def _optimizer(self) -> None:
         for ev in self._rs_events:
             self._wait(ev, "zero")
         self._join_aux(self.s_comp)  # D == 1: bias / norm grads reduced on aux feed this update
-        spec = self.spec
-        for st in self.stages.values():
-            ops.adamw(st.master, st.exp_avg, st.exp_avg_sq, st.grad_sub, st.sub_bf16, spec.lr, spec.beta1,
-                      spec.beta2, spec.adam_eps, spec.weight_decay, self.step_count, stream=self.s_comp)
+        if self._opt_ev is not None:
+            self.s_comp.wait_event(self._opt_ev)  # early chunks (overlapped with B / W) done
+        for s, st in self.stages.items():
+            if s not in self._opt_done:
+                self._adamw(st, 0, st.nsub, self.s_comp)
+                st.opt_ready = None
         if self.capture_grads:
             self.captured = {s: st.grad_sub.clone() for s, st in self.stages.items()}
         for st in self.stages.values():
@@ -745,17 +808,30 @@ class Runtime:
                 a = stash["layers"][i]
                 for dy, _, _, bias in linears:
                     ops.colsum_acc(a[dy], G[(bias, l)], self.cs_ws, accumulate=st.accumulate((bias, l)), stream=aux)
-        for i, l in enumerate(range(lo, hi)):
+        early = self.early_opt and self.D == 1 and self._final_w.get(s) == self._ti
+        after = [self._record(self.s_aux)] if early and self.s_aux is not self.s_comp else []
+
+        def chunk_done(key):  # every gradient writer of chunk ``key`` is enqueued
+            if early:
+                self._early_opt(st, key, after + [self._record(self.s_comp)])
+                after.clear()
+
+        if s == self.S - 1:
+            ops.gemm(stash["dlogits"], stash["xf"], G[("w_lm", None)], a_t=True, b_t=True,
+                     epilogue=ops.EPI_F32_ACC if st.accumulate(("w_lm", None)) else ops.EPI_F32)
+            chunk_done("head")
+        for i, l in reversed(list(enumerate(range(lo, hi)))):
             a = stash["layers"][i]
             for dy, x, w, bias in linears:
                 ops.gemm(a[dy], a[x], G[(w, l)], a_t=True, b_t=True,
                          epilogue=ops.EPI_F32_ACC if st.accumulate((w, l)) else ops.EPI_F32)
-        if s == self.S - 1:
-            ops.gemm(stash["dlogits"], stash["xf"], G[("w_lm", None)], a_t=True, b_t=True,
-                     epilogue=ops.EPI_F32_ACC if st.accumulate(("w_lm", None)) else ops.EPI_F32)
+            chunk_done(l)
         if s == 0:
             ops.embed_bwd(self._ids[m], stash["demb"], G[("wte", None)], G.get(("wpe", None)),
                           self.spec.seq_len)
+            chunk_done("embed")
+        if early:
+            self._opt_done.add(s)
 
 
 def execute(sched: Schedule, model: ModelSpec, cfg: ParallelConfig, placement: Placement,

@@ -85,6 +85,8 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     _lib = lib
+    if os.environ.get("ZPP_ATTN_IMPL"):  # A/B switch for the attention kernels (see ops.set_attn_impl)
+        check(lib.zpp_attn_set_impl(int(os.environ["ZPP_ATTN_IMPL"])), "zpp_attn_set_impl")
     return lib
 
 

@@ -187,7 +187,8 @@ def gelu(u, g, stream=None):
 
 
 def set_attn_impl(impl: int) -> None:
-    """0 auto (tcgen05 kernels when seq % 128 == 0), 1 mma.sync FlashAttention-2 tiles."""
+    """0 auto (tcgen05 kernels when seq % 128 == 0; forward with two query tiles per CTA when
+    seq % 256 == 0), 1 mma.sync FlashAttention-2 tiles, 2 tcgen05 one query tile per CTA."""
     lib.call("zpp_attn_set_impl", impl)
 
 

@@ -259,7 +259,7 @@ def _attn_ref(qkv, b, s, H, D):
     return o.transpose(1, 2).reshape(b * s, H * D), lse
 
 
-@pytest.fixture(params=[0, 1], ids=["tc", "mma"])
+@pytest.fixture(params=[0, 1, 2], ids=["tc", "mma", "tc1"])
 def attn_impl(request):
     ops.set_attn_impl(request.param)
     yield request.param
@@ -267,7 +267,7 @@ def attn_impl(request):
 
 
 @pytest.mark.parametrize("D", [64, 128])
-@pytest.mark.parametrize("b,s,H", [(1, 128, 2), (2, 256, 3), (1, 512, 2)])
+@pytest.mark.parametrize("b,s,H", [(1, 128, 2), (2, 256, 3), (1, 512, 2), (2, 1024, 3)])
 def test_attention(b, s, H, D, attn_impl):
     qkv = bf(b * s, 3 * H * D)
     out = torch.empty(b * s, H * D, device=dev, dtype=torch.bfloat16)
@@ -356,7 +356,7 @@ def test_init_param_bit_exact():
 
 
 @pytest.mark.timeout(120)
-def test_attention_divergent_rescale():
+def test_attention_divergent_rescale(attn_impl):
     """Rows of one warp needing O-rescaling at different key blocks (regression: the
     rescale branch holds warp-collective tcgen05.ld/st and must stay warp-uniform)."""
     b, s, H, D = 1, 512, 2, 128

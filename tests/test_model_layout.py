@@ -53,3 +53,25 @@ def test_oracle_step_runs(arch):
     assert abs(loss - math.log(spec.vocab)) < 0.5
     assert set(grads) == set(params) and all(torch.isfinite(v).all() for v in grads.values())
     assert all(not torch.equal(new[k], params[k]) for k in params)
+
+
+@pytest.mark.parametrize("spec", [GPTSpec.tiny(), GPTSpec.gpt_6p2b(), GPTSpec.tiny_llama()], ids=["gpt-tiny", "gpt-6.2b", "llama-tiny"])
+@pytest.mark.parametrize("P,V", [(1, 1), (2, 2)])
+def test_opt_chunks_partition_stage(spec, P, V):
+    """Early-optimizer chunks (embed / per layer / head) tile each stage buffer exactly."""
+    from paper_2402_03791_b200.engine.executor import opt_chunks
+    model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
+    cfg = ParallelConfig(pp_size=P, dp_size=1, microbatches=P, unit_size=P, stages_per_device=V)
+    pl = make_placement(cfg, model)
+    for s in range(cfg.num_stages):
+        lay = stage_layout(spec, s, cfg.num_stages, pl.stage_to_layers[s], 1, 1)
+        ch = opt_chunks(lay)
+        lo, hi = pl.stage_to_layers[s]
+        want = set(range(lo, hi)) | ({"embed"} if s == 0 else set()) | ({"head"} if s == cfg.num_stages - 1 else set())
+        assert set(ch) == want
+        spans = sorted(ch.values())
+        assert spans[0][0] == 0 and spans[-1][1] == lay.numel
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        for sl in lay.slots:
+            key = "embed" if sl.name in ("wte", "wpe") else "head" if sl.layer is None else sl.layer
+            assert ch[key][0] <= sl.offset and sl.offset + sl.numel <= ch[key][1]

@@ -20,7 +20,7 @@ def timeit(fn, iters=20):
     for _ in range(iters): fn()
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / iters
-for impl, name in ((0, "tcgen05"), (1, "mma.sync")):
+for impl, name in ((0, "tc-2tile"), (2, "tc-1tile"), (1, "mma.sync")):
     ops.set_attn_impl(impl)
     f = timeit(lambda: ops.attn_fwd(qkv, out, lse, b, s, H, D))
     bw = timeit(lambda: ops.attn_bwd(qkv, out, lse, do, dqkv, ws, b, s, H, D))
