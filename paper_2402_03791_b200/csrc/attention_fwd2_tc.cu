@@ -291,6 +291,12 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+template <int D, int EMU>
+static cudaError_t fwd2_attr() {
+  return cudaFuncSetAttribute(attn_fwd2_tc_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Fwd2Cfg<D>::SMEM);
+}
+
 template <int D>
 int attn_fwd2_tc_launch(const void* qkv, void* out, float* lse, int B, int T, int H, cudaStream_t s) {
   using C = Fwd2Cfg<D>;
@@ -307,6 +313,11 @@ int attn_fwd2_tc_launch(const void* qkv, void* out, float* lse, int B, int T, in
   if (emu < 0) {
     const char* ev = getenv("ZPP_ATTN_EMU");
     emu = ev ? atoi(ev) : kFwd2DefaultEmu;
+    cudaError_t e = emu >= 3 ? fwd2_attr<D, 3>() : emu == 2 ? fwd2_attr<D, 2>() : fwd2_attr<D, 0>();
+    if (e != cudaSuccess) {
+      emu = -1;
+      return set_cuda_error(e, "attn_fwd2_tc attr");
+    }
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   const int BH = B * H;
@@ -322,12 +333,6 @@ int attn_fwd2_tc_launch(const void* qkv, void* out, float* lse, int B, int T, in
 
 template int attn_fwd2_tc_launch<64>(const void*, void*, float*, int, int, int, cudaStream_t);
 template int attn_fwd2_tc_launch<128>(const void*, void*, float*, int, int, int, cudaStream_t);
-
-template <int D, int EMU>
-static cudaError_t fwd2_attr() {
-  return cudaFuncSetAttribute(attn_fwd2_tc_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Fwd2Cfg<D>::SMEM);
-}
 
 int attention_fwd2_preload() {
   cudaError_t e = fwd2_attr<64, 0>();

@@ -125,3 +125,26 @@ def test_outer_dp_step_matches_oracle(tmp_path, n, P, D, B, U, V, mode):
     for rank in range(world):
         txt = (tmp_path / f"rank{rank}.txt").read_text()
         assert txt.startswith("OK"), txt
+
+
+@pytest.mark.parametrize("P,D,B,U,V", [(1, 1, 4, 2, 1), (1, 1, 4, 2, 2), (2, 2, 8, 4, 2), (1, 4, 4, 2, 2),
+                                       (2, 1, 8, 4, 2)])
+def test_early_optimizer_is_bit_identical(tmp_path, P, D, B, U, V):
+    """3 steps with the early (chunked, overlapped) optimizer == 3 steps without it, bit for
+    bit: losses, fp32 masters and bf16 shards on every rank."""
+    world = P * D
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs (run via gpurun --gpus {world})")
+    here = os.path.dirname(os.path.abspath(__file__))
+    worker = os.path.join(here, "dist_worker_ab.py")
+    args = [str(x) for x in (P, D, B, U, V, 3)] + [str(tmp_path)]
+    if world == 1:
+        cmd = [sys.executable, worker] + args
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr=127.0.0.1", "--master-port=29535", worker] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for rank in range(world):
+        txt = (tmp_path / f"rank{rank}.txt").read_text()
+        assert txt.startswith("OK"), txt
