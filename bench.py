@@ -98,14 +98,17 @@ def cpu_sample(threads: int | None = None) -> dict:
 
 # --------------------------------------------------------------------------- clocks
 class Clocks:
-    def __init__(self, out_dir: str):
+    def __init__(self, out_dir: str, device: int = 0):
         self.path = os.path.join(out_dir, "clocks.csv")
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            device = int(vis.split(",")[device])
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
@@ -131,9 +134,9 @@ class Clocks:
                     reasons.add(n)
         if not sm:
             return None
-        loaded = [x for x in sm if x > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "power_w": statistics.median(pw) if pw else None}
+        loaded = [i for i, x in enumerate(sm) if x > 0.5 * mx] or list(range(len(sm)))
+        return {"sm_mhz": statistics.median(sm[i] for i in loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "power_w": statistics.median(pw[i] for i in loaded) if len(pw) == len(sm) else None}
 
 
 # --------------------------------------------------------------------------- GPU leg
@@ -154,14 +157,16 @@ def run_zpp(args) -> None:
     if world > 1:
         dist.init_process_group("gloo")
     P, D, B, U, V = _split(args)
-    spec = getattr(GPTSpec, MODELS[args.model][0])()
+    mbs = args.mb_size
+    spec = getattr(GPTSpec, MODELS[args.model][0])(microbatch_samples=mbs)
     model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
-    cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V)
+    cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V,
+                         microbatch_samples=mbs)
     pl = make_placement(cfg, model)
     sched = generate(model, cfg, pl)
     rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=True)
     z = rt.z
-    toks = make_tokens(1, D, B, 1, spec.seq_len, spec.vocab)[0]
+    toks = make_tokens(1, D, B, mbs, spec.seq_len, spec.vocab)[0]
     ids_h = toks[z, :, :, :-1].reshape(B, -1).contiguous().pin_memory()
     lab_h = toks[z, :, :, 1:].reshape(B, -1).contiguous().pin_memory()
     ids_d, lab_d = ids_h.cuda(), lab_h.cuda()
@@ -185,7 +190,7 @@ def run_zpp(args) -> None:
     barrier()
 
     # ---- kernel-resident timed region (value) ----------------------------------
-    clocks = Clocks(args.out_dir) if rank == 0 else None
+    clocks = Clocks(args.out_dir, local) if rank == 0 else None
     comp = rt.s_comp
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ops.PROFILE.start(time_gemms=False)  # launch counting only: no per-kernel events here
@@ -249,9 +254,9 @@ def run_zpp(args) -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded CPU randint tokens, deterministic counter-hash init)",
             "config": {"workload": f"{args.model.upper()} ZeroPP step, P{P} x D{D}, B={B} micro-batches/ZeRO "
-                                   f"rank, U={U}, V={V}, b=1, s={spec.seq_len}",
+                                   f"rank, U={U}, V={V}, b={mbs}, s={spec.seq_len}",
                        "model": MODELS[args.model][1],
-                       "global_batch": D * B, "seq_len": spec.seq_len, "parallelism": f"pp{P}xzero{D}",
+                       "global_batch": D * B * mbs, "seq_len": spec.seq_len, "parallelism": f"pp{P}xzero{D}",
                        "tokens_per_step": tokens_per_step,
                        "l2": "inputs larger than L2 (each step streams >10 GB of weights/activations)"},
             "mfu": {"vs_2250_dense": round(value * flops_tok / (N * PEAK_DENSE_TF * 1e12), 4),
@@ -329,6 +334,7 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--model", default="gpt-6.2b", choices=sorted(MODELS))
     ap.add_argument("--split", default=None, help="PxD:B:U:V override of the default split for --gpus")
+    ap.add_argument("--mb-size", type=int, default=1, help="samples per micro-batch (ParallelConfig.microbatch_samples)")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out"))
     args = ap.parse_args()
     os.makedirs(args.out_dir, exist_ok=True)

@@ -118,8 +118,10 @@ int zpp_gelu_fwd(const void* u, void* g, long long n, uintptr_t stream);
 /* ---- token + position embedding (stage 0) ------------------------------------ */
 int zpp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* out, int tokens, int seq,
                   int hidden, uintptr_t stream);
+/* dwte[ids[t]] += dout[t], dwpe[t % seq] += dout[t] (fp32, accumulate).  Deterministic: every
+   row's contributions are summed in token order (no atomics); vocab = rows of dwte. */
 int zpp_embed_bwd(const int64_t* ids, const void* dout, float* dwte, float* dwpe, int tokens, int seq, int hidden,
-                  uintptr_t stream);
+                  int vocab, uintptr_t stream);
 
 /* ---- fused softmax cross-entropy (last stage): logits -> dlogits in place ----- */
 /* loss_sum(f32) += sum_r CE_r ; dlogits = (softmax - onehot) * grad_scale            */

@@ -353,20 +353,75 @@ __global__ void embed_fwd_kernel(const int64_t* __restrict__ ids, const bf16* __
   }
 }
 
-__global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, const bf16* __restrict__ dout,
-                                 float* __restrict__ dwte, float* __restrict__ dwpe, int seq, int hidden) {
-  const int t = blockIdx.x;
-  float* e = dwte + ids[t] * (long long)hidden;
-  float* p = dwpe ? dwpe + (long long)(t % seq) * hidden : nullptr;
-  const bf16* d = dout + (long long)t * hidden;
-  for (int v = threadIdx.x; v < hidden / 8; v += blockDim.x) {
-    float a[8];
-    unpack8(reinterpret_cast<const uint4*>(d)[v], a);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      atomicAdd(e + v * 8 + j, a[j]);
-      if (p) atomicAdd(p + v * 8 + j, a[j]);
+// Embedding backward, deterministic (no fp32 atomics): dwte rows are owned by CTAs (a range
+// of EMB_ROWS vocabulary rows each); every CTA compacts, in token order, the tokens whose id
+// falls in its range and adds their gradient rows one after another (thread = column slice),
+// so each row's sum order is the token order whatever the scheduling.  dwpe: one CTA per
+// position sums the micro-batch's samples in order.
+constexpr int EMB_ROWS = 128;
+__global__ void __launch_bounds__(256) embed_bwd_wte_kernel(const int64_t* __restrict__ ids,
+                                                            const bf16* __restrict__ dout, float* __restrict__ dwte,
+                                                            int tokens, int hidden, int vocab) {
+  extern __shared__ int match[];  // [tokens]
+  __shared__ int warp_cnt[8];
+  __shared__ int total;
+  const int v0 = blockIdx.x * EMB_ROWS, v1 = min(vocab, v0 + EMB_ROWS);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (threadIdx.x == 0) total = 0;
+  __syncthreads();
+  for (int c = 0; c < tokens; c += 256) {
+    const int t = c + threadIdx.x;
+    const long long id = t < tokens ? ids[t] : -1;
+    const bool hit = id >= v0 && id < v1;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (l == 0) warp_cnt[w] = __popc(bal);
+    __syncthreads();
+    int off = total;
+    for (int i = 0; i < w; ++i) off += warp_cnt[i];
+    if (hit) match[off + __popc(bal & ((1u << l) - 1u))] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int sum = 0;
+      for (int i = 0; i < 8; ++i) sum += warp_cnt[i];
+      total += sum;
     }
+    __syncthreads();
+  }
+  const int n = total;
+  for (int k = 0; k < n; ++k) {
+    const int t = match[k];
+    float* e = dwte + ids[t] * (long long)hidden;
+    const bf16* d = dout + (long long)t * hidden;
+    for (int v = threadIdx.x; v < hidden / 8; v += 256) {
+      float a[8];
+      unpack8(reinterpret_cast<const uint4*>(d)[v], a);
+      float4* ep = reinterpret_cast<float4*>(e + v * 8);
+      float4 x0 = ep[0], x1 = ep[1];
+      x0.x += a[0]; x0.y += a[1]; x0.z += a[2]; x0.w += a[3];
+      x1.x += a[4]; x1.y += a[5]; x1.z += a[6]; x1.w += a[7];
+      ep[0] = x0;
+      ep[1] = x1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) embed_bwd_wpe_kernel(const bf16* __restrict__ dout, float* __restrict__ dwpe,
+                                                            int tokens, int seq, int hidden) {
+  const int pos = blockIdx.x;
+  for (int v = threadIdx.x; v < hidden / 8; v += 256) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int t = pos; t < tokens; t += seq) {
+      float a[8];
+      unpack8(reinterpret_cast<const uint4*>(dout + (long long)t * hidden)[v], a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += a[j];
+    }
+    float4* ep = reinterpret_cast<float4*>(dwpe + (long long)pos * hidden + v * 8);
+    float4 x0 = ep[0], x1 = ep[1];
+    x0.x += acc[0]; x0.y += acc[1]; x0.z += acc[2]; x0.w += acc[3];
+    x1.x += acc[4]; x1.y += acc[5]; x1.z += acc[6]; x1.w += acc[7];
+    ep[0] = x0;
+    ep[1] = x1;
   }
 }
 
@@ -513,7 +568,7 @@ int kernels_preload() {
                        (const void*)layernorm_fwd_kernel<true>, (const void*)layernorm_bwd_dx_kernel<true>,
                        (const void*)swiglu_fwd_kernel, (const void*)swiglu_bwd_kernel, (const void*)rope_kernel,
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
-                       (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_kernel,
+                       (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_wte_kernel, (const void*)embed_bwd_wpe_kernel,
                        (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel,
                        (const void*)adamw_kernel, (const void*)init_param_kernel};
   for (const void* f : fns) {
@@ -659,10 +714,22 @@ extern "C" int zpp_embed_fwd(const int64_t* ids, const void* wte, const void* wp
 }
 
 extern "C" int zpp_embed_bwd(const int64_t* ids, const void* dout, float* dwte, float* dwpe, int tokens, int seq,
-                             int hidden, uintptr_t stream) {
+                             int hidden, int vocab, uintptr_t stream) {
   if (hidden % 8) return set_error(ZPP_ERR_ARG, "embed_bwd: hidden % 8 != 0");
-  embed_bwd_kernel<<<tokens, 256, 0, STREAM(stream)>>>(ids, (const bf16*)dout, dwte, dwpe, seq, hidden);
-  return check_launch("embed_bwd");
+  const size_t smem = (size_t)tokens * sizeof(int);  // the CTA's ordered match list
+  if (smem > 200 * 1024) return set_error(ZPP_ERR_ARG, "embed_bwd: more than 51200 tokens per call");
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(embed_bwd_wte_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return set_cuda_error(e, "embed_bwd attr");
+    smem_set = 200 * 1024;
+  }
+  embed_bwd_wte_kernel<<<(vocab + EMB_ROWS - 1) / EMB_ROWS, 256, smem, STREAM(stream)>>>(ids, (const bf16*)dout, dwte,
+                                                                                       tokens, hidden, vocab);
+  int rc = check_launch("embed_bwd_wte");
+  if (rc || !dwpe) return rc;
+  embed_bwd_wpe_kernel<<<seq, 256, 0, STREAM(stream)>>>((const bf16*)dout, dwpe, tokens, seq, hidden);
+  return check_launch("embed_bwd_wpe");
 }
 
 extern "C" int zpp_xent_fwd_bwd(void* logits, long long ld, const int64_t* labels, float* loss_sum, int rows,

@@ -42,7 +42,7 @@ _SIGS = {
     "zpp_colsum_acc": (c_int, [P, c_size, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_gelu_fwd": (c_int, [P, P, c_size, c_stream]),
     "zpp_embed_fwd": (c_int, [P, P, P, P, c_int, c_int, c_int, c_stream]),
-    "zpp_embed_bwd": (c_int, [P, P, P, P, c_int, c_int, c_int, c_stream]),
+    "zpp_embed_bwd": (c_int, [P, P, P, P, c_int, c_int, c_int, c_int, c_stream]),
     "zpp_xent_fwd_bwd": (c_int, [P, c_size, P, P, c_int, c_int, c_float, c_stream]),
     "zpp_cast_scale_f32_bf16": (c_int, [P, P, c_size, c_float, c_stream]),
     "zpp_accum_bf16_f32": (c_int, [P, P, c_size, c_stream]),

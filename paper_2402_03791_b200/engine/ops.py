@@ -215,8 +215,9 @@ def embed_fwd(ids, wte, wpe, out, seq, stream=None):
 
 def embed_bwd(ids, dout, dwte, dwpe, seq, stream=None):
     tokens, hidden = dout.shape
-    _count(1)
-    lib.call("zpp_embed_bwd", _p(ids), _p(dout), _p(dwte), _p(dwpe), tokens, seq, hidden, _s(stream))
+    _count(2 if dwpe is not None else 1)
+    lib.call("zpp_embed_bwd", _p(ids), _p(dout), _p(dwte), _p(dwpe), tokens, seq, hidden, dwte.shape[0],
+             _s(stream))
 
 
 def xent(logits, labels, loss_sum, grad_scale, stream=None):
