@@ -36,7 +36,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tokens/s/box GPT-6.2B ZeroPP at 1/2/4/8 B200; MFU; exposed comm ms/step"
-SPLITS = {1: (1, 1, 8, 2, 1), 2: (2, 1, 16, 8, 2), 4: (2, 2, 16, 8, 2), 8: (2, 4, 16, 8, 2)}
+# (P, D, B, U, V, b): b = samples per micro-batch (ParallelConfig.microbatch_samples).  b = 2
+# (4096-token micro-batches) measured +10% over b = 1 at N=1 (profiles/r01c_n1_microbatch_size.txt):
+# M = 4096 GEMMs waste less per FLOP, which is what counts under the 1000 W cap (DESIGN 5a).
+SPLITS = {1: (1, 1, 8, 2, 1, 2), 2: (2, 1, 16, 8, 2, 2), 4: (2, 2, 16, 8, 2, 2), 8: (2, 4, 16, 8, 2, 2)}
 # other BASELINE configs (parity cases; measured with --model / --split, not the headline line)
 MODELS = {"gpt-6.2b": ("gpt_6p2b", "GPT-6.2B (L32 h4096 a32 s2048 V50304, untied head)"),
           "gpt-1.3b": ("gpt_1p3b", "GPT-1.3B (L24 h2048 a16 s2048 V50304, untied head)"),
@@ -156,8 +159,7 @@ def run_zpp(args) -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo")
-    P, D, B, U, V = _split(args)
-    mbs = args.mb_size
+    P, D, B, U, V, mbs = _split(args)
     spec = getattr(GPTSpec, MODELS[args.model][0])(microbatch_samples=mbs)
     model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
     cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V,
@@ -288,13 +290,19 @@ def run_zpp(args) -> None:
 
 
 def _split(args):
+    """(P, D, B, U, V, b) of --gpus, or of --split PxD:B:U:V[:b]; --mb-size overrides b."""
     if not args.split:
-        return SPLITS[args.gpus]
-    pd, B, U, V = args.split.split(":")
-    P, D = (int(x) for x in pd.lower().split("x"))
-    if P * D != args.gpus:
-        raise SystemExit(f"--split {args.split}: P*D != --gpus {args.gpus}")
-    return P, D, int(B), int(U), int(V)
+        P, D, B, U, V, b = SPLITS[args.gpus]
+    else:
+        f = args.split.split(":")
+        P, D = (int(x) for x in f[0].lower().split("x"))
+        B, U, V = int(f[1]), int(f[2]), int(f[3])
+        b = int(f[4]) if len(f) > 4 else 1
+        if P * D != args.gpus:
+            raise SystemExit(f"--split {args.split}: P*D != --gpus {args.gpus}")
+    if getattr(args, "mb_size", None):
+        b = args.mb_size
+    return P, D, B, U, V, b
 
 
 def run_reference(args) -> None:
@@ -311,12 +319,12 @@ def run_reference(args) -> None:
         vals.append(last["value"])
     total = time.perf_counter() - t0
     value = statistics.median(vals)
-    P, D, B, U, V = SPLITS[args.gpus]
+    P, D, B, U, V, mbs = _split(args)
     line = {"metric": METRIC, "impl": "reference", "value": round(value, 3), "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total / max(args.steps, 1) * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"GPT-6.2B ZeroPP step, P{P} x D{D}, B={B}, U={U}, V={V}, b=1, s=2048",
+            "config": {"workload": f"GPT-6.2B ZeroPP step, P{P} x D{D}, B={B}, U={U}, V={V}, b={mbs}, s=2048",
                        "model": "GPT-6.2B", "seq_len": 2048, "parallelism": "cpu oracle (host cores)"},
             "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": last["cores"],
                              "kind": "port", "sample": last["sample"]},
@@ -334,7 +342,8 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--model", default="gpt-6.2b", choices=sorted(MODELS))
     ap.add_argument("--split", default=None, help="PxD:B:U:V override of the default split for --gpus")
-    ap.add_argument("--mb-size", type=int, default=1, help="samples per micro-batch (ParallelConfig.microbatch_samples)")
+    ap.add_argument("--mb-size", type=int, default=None,
+                    help="samples per micro-batch (ParallelConfig.microbatch_samples); default from the split")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out"))
     args = ap.parse_args()
     os.makedirs(args.out_dir, exist_ok=True)

@@ -16,16 +16,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--B", type=int, default=8)
 ap.add_argument("--U", type=int, default=2)
+ap.add_argument("--mb", type=int, default=2, help="samples per micro-batch (bench default b=2)")
 ap.add_argument("--ncu", action="store_true")
 ap.add_argument("--gemm-shapes", default=None, help="with --ncu: write M,N,K,algorithmic bytes per GEMM launch")
 a = ap.parse_args()
-spec = GPTSpec(num_layers=a.layers, hidden=4096, heads=32, seq_len=2048)
+spec = GPTSpec(num_layers=a.layers, hidden=4096, heads=32, seq_len=2048, microbatch_samples=a.mb)
 model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
-cfg = ParallelConfig(pp_size=1, dp_size=1, microbatches=a.B, unit_size=a.U)
+cfg = ParallelConfig(pp_size=1, dp_size=1, microbatches=a.B, unit_size=a.U, microbatch_samples=a.mb)
 pl = make_placement(cfg, model)
 sched = generate(model, cfg, pl)
 rt = Runtime(spec, model, cfg, pl, sched)
-t = make_tokens(1, 1, a.B, 1, spec.seq_len, spec.vocab)[0, 0]
+t = make_tokens(1, 1, a.B, a.mb, spec.seq_len, spec.vocab)[0, 0]
 ids = t[:, :, :-1].reshape(a.B, -1).contiguous().cuda()
 lab = t[:, :, 1:].reshape(a.B, -1).contiguous().cuda()
 for _ in range(2):

@@ -28,14 +28,16 @@ rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
 if world > 1:
     dist.init_process_group("gloo")
-P, D, B, U, V = bench._split(args)
-spec = GPTSpec.gpt_6p2b()
+args.mb_size = None
+P, D, B, U, V, mb = bench._split(args)
+spec = GPTSpec.gpt_6p2b(microbatch_samples=mb)
 model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
-cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V)
+cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V,
+                     microbatch_samples=mb)
 pl = make_placement(cfg, model)
 sched = generate(model, cfg, pl)
 rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=True)
-toks = synthetic_tokens(1, D, B, 1, spec.seq_len, spec.vocab)[0]
+toks = synthetic_tokens(1, D, B, mb, spec.seq_len, spec.vocab)[0]
 ids = toks[rt.z, :, :, :-1].reshape(B, -1).contiguous().cuda()
 lab = toks[rt.z, :, :, 1:].reshape(B, -1).contiguous().cuda()
 for _ in range(args.steps):
