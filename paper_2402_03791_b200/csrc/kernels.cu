@@ -22,14 +22,15 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Block-wide sum for blockDim.x == 256 (8 warps); result broadcast to all threads.
-__device__ __forceinline__ float block_sum256(float v, float* red) {
+// Block-wide sum for blockDim.x == NT (NT / 32 warps); result broadcast to all threads.
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
   if (l == 0) red[w] = v;
   __syncthreads();
-  float t = (l < 8) ? red[l] : 0.f;
+  float t = (l < NT / 32) ? red[l] : 0.f;
   t = warp_sum(t);
   return t;
 }
@@ -43,16 +44,17 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 }
 
 // ----------------------------------------------------------------------------
-// LayerNorm: one 256-thread block per row, row cached in registers (cols <= 8192).
+// LayerNorm: one NT-thread block per row, row cached in registers (cols <= 8 * LN_VPT * NT).
+// NT = 128 for rows of <= 4096 columns: 4 vectors in flight per thread and 16 rows per SM.
 constexpr int LN_VPT = 4;  // uint4 (8 bf16) vectors per thread
 
 // RMS = true: RMSNorm (LLaMA): mean fixed at 0, no beta; mean_out may be null.
-template <bool RMS>
-__global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+template <bool RMS, int NT>
+__global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
                                                             const bf16* __restrict__ b, bf16* __restrict__ y,
                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                             int cols, float eps) {
-  __shared__ float red[8];
+  __shared__ float red[NT / 32];
   const int row = blockIdx.x;
   const bf16* xr = x + (long long)row * cols;
   const int nvec = cols / 8;
@@ -60,28 +62,28 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * 256;
+    const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), v[i]);
 #pragma unroll
       for (int j = 0; j < 8; ++j) s += v[i][j];
     }
   }
-  const float mean = RMS ? 0.f : block_sum256(s, red) / cols;
+  const float mean = RMS ? 0.f : block_sum<NT>(s, red) / cols;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * 256;
+    const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) { const float d = v[i][j] - mean; q += d * d; }
     }
   }
-  const float rstd = rsqrtf(block_sum256(q, red) / cols + eps);
+  const float rstd = rsqrtf(block_sum<NT>(q, red) / cols + eps);
   bf16* yr = y + (long long)row * cols;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * 256;
+    const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       float gg[8], bb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
       unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg);
@@ -100,28 +102,30 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const bf16* __restri
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
 // the two row sums fused into a single float2 block reduction.  RMS: mean = 0 and the
 // mean(dy*g) term drops (xhat = x * rstd).
-template <bool RMS>
-__global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                                               const float* __restrict__ mean,
-                                                               const float* __restrict__ rstd,
-                                                               const bf16* __restrict__ g, const bf16* __restrict__ dres,
-                                                               bf16* __restrict__ dx, int cols) {
-  __shared__ float2 red[8];
+template <bool RMS, int NT>
+__global__ void __launch_bounds__(NT) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                              const float* __restrict__ mean,
+                                                              const float* __restrict__ rstd,
+                                                              const bf16* __restrict__ g, const bf16* __restrict__ dres,
+                                                              bf16* __restrict__ dx, int cols) {
+  __shared__ float2 red[NT / 32];
   const int row = blockIdx.x;
   const int nvec = cols / 8;
   const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
   const bf16* xr = x + (long long)row * cols;
   const bf16* dyr = dy + (long long)row * cols;
   float xh[LN_VPT][8], dg[LN_VPT][8];
+  uint4 rv[LN_VPT];  // residual-gradient vectors, loaded with x / dy (more bytes in flight)
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * 256;
+    const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       float xv[8], dv[8], gv[8];
       unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), xv);
       unpack8(*reinterpret_cast<const uint4*>(dyr + vi * 8), dv);
       unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gv);
+      if (dres) rv[i] = *reinterpret_cast<const uint4*>(dres + (long long)row * cols + vi * 8);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         xh[i][j] = (xv[j] - mu) * rs;
@@ -141,21 +145,21 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(const bf16* __res
   __syncthreads();
   float2 t = red[0];
 #pragma unroll
-  for (int i = 1; i < 8; ++i) { t.x += red[i].x; t.y += red[i].y; }
+  for (int i = 1; i < NT / 32; ++i) { t.x += red[i].x; t.y += red[i].y; }
   const float m1 = RMS ? 0.f : t.x / cols, m2 = t.y / cols;
   bf16* dxr = dx + (long long)row * cols;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * 256;
+    const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       float o[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) o[j] = rs * (dg[i][j] - m1 - xh[i][j] * m2);
       if (dres) {
-        float rv[8];
-        unpack8(*reinterpret_cast<const uint4*>(dres + (long long)row * cols + vi * 8), rv);
+        float r[8];
+        unpack8(rv[i], r);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] += rv[j];
+        for (int j = 0; j < 8; ++j) o[j] += r[j];
       }
       *reinterpret_cast<uint4*>(dxr + vi * 8) = pack8(o);
     }
@@ -564,8 +568,10 @@ static int grid_for(long long n, int per_block) {
 
 int kernels_preload() {
   cudaFuncAttributes fa;
-  const void* fns[] = {(const void*)layernorm_fwd_kernel<false>, (const void*)layernorm_bwd_dx_kernel<false>,
-                       (const void*)layernorm_fwd_kernel<true>, (const void*)layernorm_bwd_dx_kernel<true>,
+  const void* fns[] = {(const void*)layernorm_fwd_kernel<false, 128>, (const void*)layernorm_bwd_dx_kernel<false, 128>,
+                       (const void*)layernorm_fwd_kernel<true, 128>, (const void*)layernorm_bwd_dx_kernel<true, 128>,
+                       (const void*)layernorm_fwd_kernel<false, 256>, (const void*)layernorm_bwd_dx_kernel<false, 256>,
+                       (const void*)layernorm_fwd_kernel<true, 256>, (const void*)layernorm_bwd_dx_kernel<true, 256>,
                        (const void*)swiglu_fwd_kernel, (const void*)swiglu_bwd_kernel, (const void*)rope_kernel,
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_wte_kernel, (const void*)embed_bwd_wpe_kernel,
@@ -584,12 +590,17 @@ using namespace zpp;
 
 #define STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
+// 128 threads per row when the row fits in 4 vectors per thread, else 256
+#define LN_DISPATCH(cols, KERNEL, RMSV, ...)                                                 \
+  ((cols) <= 128 * 8 * LN_VPT ? (KERNEL<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
+                              : (KERNEL<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
+
 extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  layernorm_fwd_kernel<false><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, (const bf16*)beta,
-                                                          (bf16*)y, mean, rstd, cols, eps);
+  LN_DISPATCH(cols, layernorm_fwd_kernel, false, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean,
+              rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
 
@@ -622,8 +633,8 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  layernorm_bwd_dx_kernel<false><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
-                                                             (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx, cols);
+  LN_DISPATCH(cols, layernorm_bwd_dx_kernel, false, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
+              (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc || !dgamma) return rc;  // dgamma == null: parameter grads via zpp_norm_param_grads
   return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, accumulate,
@@ -634,8 +645,8 @@ extern "C" int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float*
                                uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  layernorm_fwd_kernel<true><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y,
-                                                               nullptr, rstd, cols, eps);
+  LN_DISPATCH(cols, layernorm_fwd_kernel, true, (const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y, nullptr, rstd,
+              cols, eps);
   return check_launch("rmsnorm_fwd");
 }
 
@@ -645,9 +656,8 @@ extern "C" int zpp_rmsnorm_bwd(const void* dy, const void* x, const float* rstd,
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  layernorm_bwd_dx_kernel<true><<<rows, 256, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, nullptr, rstd,
-                                                                  (const bf16*)gamma, (const bf16*)dresid, (bf16*)dx,
-                                                                  cols);
+  LN_DISPATCH(cols, layernorm_bwd_dx_kernel, true, (const bf16*)dy, (const bf16*)x, nullptr, rstd, (const bf16*)gamma,
+              (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("rmsnorm_bwd_dx");
   if (rc || !dgamma) return rc;
   return colred_launch(true, dy, cols, x, nullptr, rstd, dgamma, nullptr, workspace, rows, cols, accumulate,
