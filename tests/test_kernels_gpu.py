@@ -95,6 +95,20 @@ def test_gemm_gelu_and_dgelu(cta_group):
     assert rel_err(D, u.grad) < 1e-2
 
 
+@pytest.mark.parametrize("shape", [(4096, 4096, 8192), (4352, 3840, 8192), (8192, 2048, 8192)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_gemm_grouped_raster(shape, cta_group):
+    """K-heavy shapes where neither operand fits in L2 walk the tiles in bands of 8 panels
+    (gemm.cu tile_coords): every output tile is still produced exactly once."""
+    M, N, K = shape
+    A, B = bf(M, K), bf(N, K)
+    C = torch.full((M, N), float("nan"), device=dev, dtype=torch.float32)
+    ops.gemm(A, B, C, epilogue=ops.EPI_F32)
+    ref = A.float() @ B.float().t()
+    assert not torch.isnan(C).any()
+    assert rel_err(C, ref) < 1e-5 * math.sqrt(K) + 1e-5
+
+
 # Shapes whose last wave is split into stream-K pieces at 148 SMs (74 pairs):
 # 2048x4096 -> 128 pair tiles (74 whole + 54 x 4 pieces); 2048x12288 -> 384 (370 + 14 x p).
 SK_SHAPES = [(2048, 4096, 4096), (2048, 12288, 1024), (2048, 4096, 16384), (1000, 4000, 2048)]
