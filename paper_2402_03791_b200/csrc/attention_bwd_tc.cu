@@ -189,43 +189,35 @@ __global__ void __launch_bounds__(384, 1)
       }
       mbar_wait(sp_full, it & 1);
       tc_fence_after();
-      // P^T and dS^T of this query block in registers first: only the dS^T smem stores have
-      // to wait for dK(it-1) to finish reading the buffer, so this overlaps dK(it-1)
-      uint32_t dsp[2][16];
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {  // 32 queries per chunk, this warp's half
-        const int c = 2 * hh + cc;
+      if (it > 0) mbar_wait(ds_free, (it - 1) & 1);  // dK(it-1) finished reading dS^T smem
+#pragma unroll 1
+      for (int c = 2 * hh; c < 2 * hh + 2; ++c) {  // 32 queries per chunk, this warp's half
         uint32_t sv[32], pv[32];
         tmem_ld32(T_S + lo + c * 32, sv);
         tmem_ld32(T_DP + lo + c * 32, pv);
         tmem_wait_ld();
+        float p[32], ds[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int qi = c * 32 + j;
+          float pj = fast_exp2(__uint_as_float(sv[j]) * sl2 - sL[qi]);
+          if (it == 0 && r > qi) pj = 0.f;  // diagonal block: key after query
+          p[j] = pj;
+          ds[j] = pj * (__uint_as_float(pv[j]) - sDl[qi]) * scale;
+        }
         uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const int qi = c * 32 + j;
-          float p0 = fast_exp2(__uint_as_float(sv[j]) * sl2 - sL[qi]);
-          float p1 = fast_exp2(__uint_as_float(sv[j + 1]) * sl2 - sL[qi + 1]);
-          if (it == 0 && r > qi) p0 = 0.f;  // diagonal block: key after query
-          if (it == 0 && r > qi + 1) p1 = 0.f;
-          pk[j / 2] = pack_bf16(p0, p1);
-          dsp[cc][j / 2] = pack_bf16(p0 * (__uint_as_float(pv[j]) - sDl[qi]) * scale,
-                                     p1 * (__uint_as_float(pv[j + 1]) - sDl[qi + 1]) * scale);
-        }
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
         // P^T bf16 over the S^T columns this warp already consumed (each column half packs into
-        // its own first 32 columns, so the other half's scores are never overwritten); dV(it-1)
-        // read the previous P^T before S^T(it) was computed into these columns
+        // its own first 32 columns, so the other half's scores are never overwritten)
         tmem_st16(T_S + lo + (c >> 1) * 64 + (c & 1) * 16, pk);
-      }
-      if (it > 0) mbar_wait(ds_free, (it - 1) & 1);  // dK(it-1) finished reading dS^T smem
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = 2 * hh + cc;
         const uint32_t rowp = base + C::DS_OFF + (c >> 1) * C::ATOM + r * 128;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int c8 = (c & 1) * 4 + t;
-          st_shared_v4(rowp + ((c8 ^ (r & 7)) << 4), dsp[cc][4 * t], dsp[cc][4 * t + 1], dsp[cc][4 * t + 2],
-                       dsp[cc][4 * t + 3]);
+          const float* s = &ds[t * 8];
+          st_shared_v4(rowp + ((c8 ^ (r & 7)) << 4), pack_bf16(s[0], s[1]), pack_bf16(s[2], s[3]),
+                       pack_bf16(s[4], s[5]), pack_bf16(s[6], s[7]));
         }
       }
       tmem_wait_st();
