@@ -281,7 +281,7 @@ def run_zpp(args) -> None:
             "gpu_launches": launches,
             "clocks": clk,
         }
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # the CPU baseline is an N=1 leg (rank 0 only)
             line["cpu_baseline"] = cpu_sample()
         print(json.dumps(line), flush=True)
     if world > 1:
