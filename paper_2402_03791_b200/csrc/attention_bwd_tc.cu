@@ -259,9 +259,10 @@ __global__ void __launch_bounds__(384, 1)
 
 // ---------------------------------------------------------------------------------------
 // dQ.  warp 0: TMA (Q_i, dO_i once; K_j ring of 3 -- K is read by S_j and dQ_j), warp 3:
-// TMA V_j ring of 2, warp 1: MMA issuer, warp 2: TMEM owner, warps 4..7: thread = query row.
-// TMEM: S_j double buffer [0,256) (dS_j bf16 written over S_j's first 64 columns),
-// dP [256,384), dQ [384,512).
+// TMA V_j ring of 2, warp 1: MMA issuer, warp 2: TMEM owner, warps 4..11: thread = query
+// row, warp (q, hh) takes key-column half hh (2 softmax warps per SM sub-partition).
+// TMEM: S_j double buffer [0,256) (dS_j bf16: each 64-key half packed over the first 32 of
+// its own S columns), dP [256,384), dQ [384,512).
 // Per key block j the row threads compute P = exp2(S*scale*log2e - lse*log2e) as soon as
 // S_j lands, then wait for dP_j, form dS = P (dP - delta) * scale into TMEM and signal; the
 // MMA warp then issues dP_{j+1} (dP's columns are free) and dQ += dS_j K_j, with S_{j+1}
@@ -281,7 +282,7 @@ struct DqCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                           const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
                           int T, int H, float scale) {
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(s_full0 + 8 * s, 1);
     }
     mbar_init(dp_full, 1);
-    mbar_init(ds_full, 128);
+    mbar_init(ds_full, 256);
     mbar_init(dq_done, 1);
     fence_mbar_init();
   }
@@ -401,52 +402,50 @@ __global__ void __launch_bounds__(256, 1)
         if (j + 1 < nkb) issue_dp(j + 1);  // the row threads have read dP_j
         const uint32_t kb = base + C::K_OFF + (j % C::KST) * C::TILE;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dQ += dS K : A = dS (TMEM, 8 packed columns per k16)
-          mma_bf16_ts(T_DQ, T_S + (j & 1) * 128 + kk * 8, make_sdesc(kb + kk * 2048, C::ATOM, 1024), id_q,
-                      (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 8; ++kk)  // dQ += dS K : A = dS (TMEM; each 64-key half packed in its first 32 columns)
+          mma_bf16_ts(T_DQ, T_S + (j & 1) * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
+                      make_sdesc(kb + kk * 2048, C::ATOM, 1024), id_q, (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit(k_empty0 + 8 * (j % C::KST));
       }
       mma_commit(dq_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
+    // 8 warps: warp (q, hh) owns TMEM lane quarter q (query rows) and key-column half hh
     const int q = warp & 3;
+    const int hh = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // query row == TMEM lane
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * kLog2e;
     const float lse_r = lse[(long long)bh * T + q0 + r] * kLog2e;
     const float del_r = delta[(long long)bh * T + q0 + r];
     for (int j = 0; j < nkb; ++j) {
-      const uint32_t ts = T_S + lo + (j & 1) * 128;
+      const uint32_t ts = T_S + lo + (j & 1) * 128 + hh * 64;
       mbar_wait(s_full0 + 8 * (j & 1), (j >> 1) & 1);
       tc_fence_after();
-      float p[128];
+      float p[64];
       {
-        uint32_t v0[32], v1[32], v2[32], v3[32];
+        uint32_t v0[32], v1[32];
         tmem_ld32(ts, v0);
         tmem_ld32(ts + 32, v1);
-        tmem_ld32(ts + 64, v2);
-        tmem_ld32(ts + 96, v3);
         tmem_wait_ld();
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           p[k] = fast_exp2(__uint_as_float(v0[k]) * sl2 - lse_r);
           p[32 + k] = fast_exp2(__uint_as_float(v1[k]) * sl2 - lse_r);
-          p[64 + k] = fast_exp2(__uint_as_float(v2[k]) * sl2 - lse_r);
-          p[96 + k] = fast_exp2(__uint_as_float(v3[k]) * sl2 - lse_r);
         }
       }
       if (j == nkb - 1) {  // diagonal block: keys after the query
 #pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if (k > r) p[k] = 0.f;
+        for (int k = 0; k < 64; ++k)
+          if (hh * 64 + k > r) p[k] = 0.f;
       }
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld32(T_DP + lo + c * 32, v);
+        tmem_ld32(T_DP + lo + hh * 64 + c * 32, v);
         tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
@@ -455,7 +454,9 @@ __global__ void __launch_bounds__(256, 1)
           const float d1 = p[c * 32 + 2 * k + 1] * (__uint_as_float(v[2 * k + 1]) - del_r) * scale;
           pk[k] = pack_bf16(d0, d1);
         }
-        tmem_st16(ts + c * 16, pk);  // dS chunk over S columns already consumed
+        // dS of this half's 64 keys packed into the half's first 32 columns, over S values
+        // this warp has already read (the other half's columns are never touched)
+        tmem_st16(ts + c * 16, pk);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     bf16* dq = dqkv + ((long long)row_base + q0 + r) * 3 * H * D + (long long)h * D;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = hh * (D / 64); c < (hh + 1) * (D / 64); ++c) {
       uint32_t v[32];
       tmem_ld32(T_DQ + lo + c * 32, v);
       tmem_wait_ld();
@@ -518,7 +519,7 @@ int attn_bwd_split_tc_launch(const void* qkv, const void* dout, const float* lse
                                                                                    H, scale);
   int rc = check_launch("attn_bwd_dkdv_tc");
   if (rc) return rc;
-  attn_bwd_dq_tc_kernel<D><<<dim3(T / 128, B * H), 256, DqCfg<D>::SMEM, s>>>(mq, mdo, lse, delta, (bf16*)dqkv, T, H,
+  attn_bwd_dq_tc_kernel<D><<<dim3(T / 128, B * H), 384, DqCfg<D>::SMEM, s>>>(mq, mdo, lse, delta, (bf16*)dqkv, T, H,
                                                                              scale);
   return check_launch("attn_bwd_dq_tc");
 }
