@@ -223,7 +223,11 @@ class Runtime:
         # gradients are final (its last W at D == 1, layer by layer; its last RS_GRAD at
         # D > 1), overlapping the remaining B / W work instead of trailing the step.  The OPT
         # task still orders everything after it (ZPP_EARLY_OPT=0: OPT runs it all, as before).
-        self.early_opt = self.n == 1 and os.environ.get("ZPP_EARLY_OPT", "1") != "0"
+        # Default on at D > 1, where it lets the next step's AG_PARAM of a stage start early;
+        # at D == 1 there is nothing to overlap but the GEMMs, which under the power cap only
+        # slows them (measured: profiles/r01c_ab_n1_aux_earlyopt_b2.txt), so it is off there.
+        mode = os.environ.get("ZPP_EARLY_OPT", "auto")
+        self.early_opt = self.n == 1 and (mode == "1" or (mode == "auto" and self.D > 1))
         self.s_opt = mk()
         self._final_w, self._final_rs = {}, {}
         for i, t in enumerate(self.tasks):
