@@ -208,12 +208,14 @@ def run_zpp(args) -> None:
     dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
 
     # ---- roofline timed region: same steps, every GEMM bracketed by CUDA events ---
+    graph_mode, rt.graph_mode = rt.graph_mode, False  # per-GEMM events need eager launches
     ops.PROFILE.start(time_gemms=True)
     barrier()
     for _ in range(args.steps):
         rt.step(ids_d, lab_d)
     barrier()
     gemm_flops, gemm_ms, gemm_calls = ops.PROFILE.stop()
+    rt.graph_mode = graph_mode
     clk = clocks.stop() if clocks else None
     # per-step exposed comm from the last step's timeline (max over ranks)
     last = rt.finish_timing(results[-1])
@@ -260,6 +262,7 @@ def run_zpp(args) -> None:
                        "model": MODELS[args.model][1],
                        "global_batch": D * B * mbs, "seq_len": spec.seq_len, "parallelism": f"pp{P}xzero{D}",
                        "tokens_per_step": tokens_per_step,
+                       "cuda_graph": rt._graph is not None,
                        "l2": "inputs larger than L2 (each step streams >10 GB of weights/activations)"},
             "mfu": {"vs_2250_dense": round(value * flops_tok / (N * PEAK_DENSE_TF * 1e12), 4),
                     f"vs_{kind}_{sustained}": round(value * flops_tok / (N * sustained * 1e12), 4)},

@@ -229,6 +229,13 @@ class Runtime:
         mode = os.environ.get("ZPP_EARLY_OPT", "auto")
         self.early_opt = self.n == 1 and (mode == "1" or (mode == "auto" and self.D > 1))
         self.s_opt = mk()
+        # CUDA-graph mode (ZPP_CUDA_GRAPH=1; one rank, no early optimizer): the task list up to
+        # OPT is captured once, on the second step, and replayed; OPT runs eagerly after it
+        # (AdamW's bias correction depends on the step number).  Shapes, buffers and the task
+        # order are static, so a replay is the same launches without the host in the loop.
+        self.graph_mode = (os.environ.get("ZPP_CUDA_GRAPH", "0") == "1" and world == 1
+                           and cfg.inter_node_dp == 1)
+        self._graph = None
         self._final_w, self._final_rs = {}, {}
         for i, t in enumerate(self.tasks):
             if t.kind is TaskKind.W:
@@ -341,6 +348,8 @@ class Runtime:
         self._rs_events: list = []
         self._grad_scale = 1.0 / (self.n * self.D * B * b * s_len)
         self.step_count += 1
+        if self.graph_mode and not self.early_opt and self.step_count >= 2 and self.tasks[-1].kind is TaskKind.OPT:
+            return self._graph_step(ids, labels)
         times = {}
         comp = self.s_comp
         comp.wait_stream(torch.cuda.current_stream(self.dev))
@@ -366,6 +375,52 @@ class Runtime:
         torch.cuda.current_stream(self.dev).wait_stream(comp)
         self._t = (t_start, t_end, times)
         tokens_done = B * b * s_len if (self.S - 1) in self.stages else 0
+        return StepResult(self.loss_sum, tokens_done)
+
+    def _graph_step(self, ids: torch.Tensor, labels: torch.Tensor) -> StepResult:
+        comp = self.s_comp
+        n_graph = len(self.tasks) - 1  # everything but the trailing OPT
+        if self._graph is None:
+            self._g_ids, self._g_labels = ids, labels  # the graph reads these buffers
+            torch.cuda.synchronize(self.dev)
+            torch.cuda.empty_cache()  # the eager steps' cached blocks would double the peak
+            saved = (ops.PROFILE.active, ops.PROFILE.time_gemms, ops.PROFILE.launches)
+            ops.PROFILE.active, ops.PROFILE.time_gemms, ops.PROFILE.launches = True, False, 0
+            timeline, self.timeline = self.timeline, False
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g, stream=comp):
+                    ops.zero(self.loss_sum, stream=comp)
+                    self._opt_done, self._opt_ev = set(), None
+                    for ti in range(n_graph):
+                        self._ti = ti
+                        self._run(self.tasks[ti])
+                    self._join_aux(comp)
+            finally:
+                self.timeline = timeline
+                self._graph_launches = ops.PROFILE.launches
+                ops.PROFILE.active, ops.PROFILE.time_gemms, ops.PROFILE.launches = saved
+            self._graph = g
+        else:
+            if ids.data_ptr() != self._g_ids.data_ptr():
+                self._g_ids.copy_(ids)
+            if labels.data_ptr() != self._g_labels.data_ptr():
+                self._g_labels.copy_(labels)
+            self._ids, self._labels = self._g_ids, self._g_labels
+        comp.wait_stream(torch.cuda.current_stream(self.dev))
+        t_start = self._record(comp, True)
+        with torch.cuda.stream(comp):
+            self._graph.replay()
+            ops._count(self._graph_launches)
+            self._opt_done, self._opt_ev = set(), None
+            for ti in range(n_graph, len(self.tasks)):
+                self._ti = ti
+                self._run(self.tasks[ti])
+        t_end = self._record(comp, True)
+        torch.cuda.current_stream(self.dev).wait_stream(comp)
+        self._t = (t_start, t_end, {})
+        spec, cfg = self.spec, self.cfg
+        tokens_done = cfg.microbatches * spec.tokens_per_microbatch if (self.S - 1) in self.stages else 0
         return StepResult(self.loss_sum, tokens_done)
 
     def finish_timing(self, res: StepResult) -> StepResult:
@@ -852,7 +907,7 @@ def execute(sched: Schedule, model: ModelSpec, cfg: ParallelConfig, placement: P
     res = runtime.step(ids, labels)
     res = runtime.finish_timing(res)
     res.host_s = time.perf_counter() - t0
-    if runtime.timeline:
+    if runtime.timeline and res.task_times:  # (a CUDA-graph replay carries no per-task times)
         from .timeline import measured_result
         import torch.distributed as dist
         gather = runtime.world > 1 and dist.is_available() and dist.is_initialized()
