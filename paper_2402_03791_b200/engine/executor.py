@@ -382,6 +382,8 @@ class Runtime:
         n_graph = len(self.tasks) - 1  # everything but the trailing OPT
         if self._graph is None:
             self._g_ids, self._g_labels = ids, labels  # the graph reads these buffers
+            import gc
+            gc.collect()
             torch.cuda.synchronize(self.dev)
             torch.cuda.empty_cache()  # the eager steps' cached blocks would double the peak
             saved = (ops.PROFILE.active, ops.PROFILE.time_gemms, ops.PROFILE.launches)
