@@ -49,75 +49,53 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 constexpr int LN_VPT = 4;  // uint4 (8 bf16) vectors per thread
 
 // RMS = true: RMSNorm (LLaMA): mean fixed at 0, no beta; mean_out may be null.
-// Each block normalises LN_ROWS consecutive rows: gamma / beta are read once per block (not
-// once per row), and the next row's x is loaded before the current row's reductions, so a
-// row's load latency overlaps the previous row's reduce + store.
-constexpr int LN_ROWS = 4;
 template <bool RMS, int NT>
 __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
                                                             const bf16* __restrict__ b, bf16* __restrict__ y,
                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
-                                                            int rows, int cols, float eps) {
+                                                            int cols, float eps) {
   __shared__ float red[NT / 32];
+  const int row = blockIdx.x;
+  const bf16* xr = x + (long long)row * cols;
   const int nvec = cols / 8;
-  const int r0 = blockIdx.x * LN_ROWS, r1 = min(rows, r0 + LN_ROWS);
-  uint4 gq[LN_VPT], bq[LN_VPT], nxt[LN_VPT];
+  float v[LN_VPT][8];
+  float s = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
-      gq[i] = *reinterpret_cast<const uint4*>(g + vi * 8);
-      bq[i] = RMS ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4*>(b + vi * 8);
-      nxt[i] = *reinterpret_cast<const uint4*>(x + (long long)r0 * cols + vi * 8);
+      unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), v[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[i][j];
     }
   }
-  for (int row = r0; row < r1; ++row) {
-    float v[LN_VPT][8];
-    float s = 0.f;
+  const float mean = RMS ? 0.f : block_sum<NT>(s, red) / cols;
+  float q = 0.f;
 #pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * NT;
-      if (vi < nvec) {
-        unpack8(nxt[i], v[i]);
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s += v[i][j];
-      }
+      for (int j = 0; j < 8; ++j) { const float d = v[i][j] - mean; q += d * d; }
     }
-    if (row + 1 < r1) {  // prefetch the next row
+  }
+  const float rstd = rsqrtf(block_sum<NT>(q, red) / cols + eps);
+  bf16* yr = y + (long long)row * cols;
 #pragma unroll
-      for (int i = 0; i < LN_VPT; ++i) {
-        const int vi = threadIdx.x + i * NT;
-        if (vi < nvec) nxt[i] = *reinterpret_cast<const uint4*>(x + (long long)(row + 1) * cols + vi * 8);
-      }
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) {
+      float gg[8], bb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
+      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg);
+      if (!RMS) unpack8(*reinterpret_cast<const uint4*>(b + vi * 8), bb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mean) * rstd * gg[j] + bb[j];
+      *reinterpret_cast<uint4*>(yr + vi * 8) = pack8(o);
     }
-    const float mean = RMS ? 0.f : block_sum<NT>(s, red) / cols;
-    float q = 0.f;
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * NT;
-      if (vi < nvec) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { const float d = v[i][j] - mean; q += d * d; }
-      }
-    }
-    const float rstd = rsqrtf(block_sum<NT>(q, red) / cols + eps);
-    bf16* yr = y + (long long)row * cols;
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * NT;
-      if (vi < nvec) {
-        float gg[8], bb[8], o[8];
-        unpack8(gq[i], gg);
-        unpack8(bq[i], bb);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mean) * rstd * gg[j] + bb[j];
-        *reinterpret_cast<uint4*>(yr + vi * 8) = pack8(o);
-      }
-    }
-    if (threadIdx.x == 0) {
-      if (!RMS) mean_out[row] = mean;
-      rstd_out[row] = rstd;
-    }
+  }
+  if (threadIdx.x == 0) {
+    if (!RMS) mean_out[row] = mean;
+    rstd_out[row] = rstd;
   }
 }
 
@@ -266,7 +244,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
 
 static int colred_splits(int rows, int strips) {
   int s = 1;
-  while (s < CR_MAX_SPLIT && strips * s < 4 * num_sms() && rows / (2 * s) >= 64) s *= 2;
+  while (s < CR_MAX_SPLIT && strips * s < 2 * num_sms() && rows / (2 * s) >= 64) s *= 2;
   return s;
 }
 
@@ -613,17 +591,16 @@ using namespace zpp;
 #define STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
 // 128 threads per row when the row fits in 4 vectors per thread, else 256
-#define LN_DISPATCH_G(grid, cols, KERNEL, RMSV, ...)                                          \
-  ((cols) <= 128 * 8 * LN_VPT ? (KERNEL<RMSV, 128><<<(grid), 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
-                              : (KERNEL<RMSV, 256><<<(grid), 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
-#define LN_DISPATCH(cols, KERNEL, RMSV, ...) LN_DISPATCH_G(rows, cols, KERNEL, RMSV, __VA_ARGS__)
+#define LN_DISPATCH(cols, KERNEL, RMSV, ...)                                                 \
+  ((cols) <= 128 * 8 * LN_VPT ? (KERNEL<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
+                              : (KERNEL<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
 
 extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH_G((rows + LN_ROWS - 1) / LN_ROWS, cols, layernorm_fwd_kernel, false, (const bf16*)x, (const bf16*)gamma,
-                (const bf16*)beta, (bf16*)y, mean, rstd, rows, cols, eps);
+  LN_DISPATCH(cols, layernorm_fwd_kernel, false, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean,
+              rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
 
@@ -668,8 +645,8 @@ extern "C" int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float*
                                uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH_G((rows + LN_ROWS - 1) / LN_ROWS, cols, layernorm_fwd_kernel, true, (const bf16*)x, (const bf16*)gamma,
-                nullptr, (bf16*)y, nullptr, rstd, rows, cols, eps);
+  LN_DISPATCH(cols, layernorm_fwd_kernel, true, (const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y, nullptr, rstd,
+              cols, eps);
   return check_launch("rmsnorm_fwd");
 }
 
