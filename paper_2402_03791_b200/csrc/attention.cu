@@ -242,25 +242,31 @@ template <int D>
 // backward kernels reduce-add into it), so no separate memset is launched.
 __global__ void attn_delta_kernel(const bf16* __restrict__ out, const bf16* __restrict__ dout,
                                   float* __restrict__ delta, float* __restrict__ dq, int B, int T, int H) {
-  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= (long long)B * T * H) return;
+  // D/8 threads per (token, head): one 16-byte vector of O and of dO each, reduced over the
+  // D/8 lanes with shuffles (full-sector coalesced loads, 32 B in flight per thread)
+  constexpr int L = D / 8;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long w = tid / L;
+  const int c = static_cast<int>(tid % L);
+  const bool ok = w < (long long)B * T * H;
+  float acc = 0.f;
+  if (ok) {
+    const uint4 ov = reinterpret_cast<const uint4*>(out + w * D)[c];
+    const uint4 dv = reinterpret_cast<const uint4*>(dout + w * D)[c];
+    acc = bf16lo(ov.x) * bf16lo(dv.x) + bf16hi(ov.x) * bf16hi(dv.x) + bf16lo(ov.y) * bf16lo(dv.y) +
+          bf16hi(ov.y) * bf16hi(dv.y) + bf16lo(ov.z) * bf16lo(dv.z) + bf16hi(ov.z) * bf16hi(dv.z) +
+          bf16lo(ov.w) * bf16lo(dv.w) + bf16hi(ov.w) * bf16hi(dv.w);
+  }
+#pragma unroll
+  for (int x = L / 2; x > 0; x >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, x);
+  if (!ok) return;
   const int h = w % H;
   const long long bt = w / H;
   const int t = bt % T, b = bt / T;
-  const bf16* o = out + w * D;
-  const bf16* d = dout + w * D;
-  float acc = 0.f;
-  for (int i = lane * 2; i < D; i += 64) {
-    const uint32_t ov = *reinterpret_cast<const uint32_t*>(o + i), dv = *reinterpret_cast<const uint32_t*>(d + i);
-    acc += bf16lo(ov) * bf16lo(dv) + bf16hi(ov) * bf16hi(dv);
-  }
-#pragma unroll
-  for (int x = 16; x > 0; x >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, x);
-  if (lane == 0) delta[((long long)b * H + h) * T + t] = acc;
+  if (c == 0) delta[((long long)b * H + h) * T + t] = acc;
   if (!dq) return;
   float4* z = reinterpret_cast<float4*>(dq + w * D);
-  for (int i = lane; i < D / 4; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = c; i < D / 4; i += L) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // ---------------------------------------------------------------------------
@@ -487,8 +493,8 @@ static int attn_bwd_launch(const void* qkv, const void* out, const float* lse, c
   const long long nrows = (long long)B * T;
   const long long warps = nrows * H;
   const bool split = use_tc && bwd_split();
-  attn_delta_kernel<D><<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>((const bf16*)out, (const bf16*)dout, delta,
-                                                                      split ? nullptr : dq, B, T, H);
+  attn_delta_kernel<D><<<(int)((warps * (D / 8) + 255) / 256), 256, 0, s>>>((const bf16*)out, (const bf16*)dout,
+                                                                           delta, split ? nullptr : dq, B, T, H);
   int rc = check_launch("attn_delta");
   if (rc) return rc;
   if (split) return attn_bwd_split_tc_launch<D>(qkv, dout, lse, delta, dqkv, B, T, H, s);

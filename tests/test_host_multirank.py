@@ -22,7 +22,7 @@ def test_rank_coords_bijective(n, P, D):
         rank_coords(n * P * D, n, P, D)
 
 
-@pytest.mark.parametrize("n,P,D", [(1, 2, 2), (1, 4, 2), (2, 2, 2), (2, 1, 4), (4, 2, 1), (1, 1, 8)])
+@pytest.mark.parametrize("n,P,D", [(1, 2, 2), (1, 2, 4), (1, 4, 2), (2, 2, 2), (2, 1, 4), (4, 2, 1), (1, 1, 8)])
 def test_comm_plan_keys_unique_per_rank(n, P, D):
     """A rank looks communicators up by node-local key: it must belong to at most one
     group per key, groups must stay inside one node (except "inter")."""
