@@ -8,7 +8,6 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "ptx.cuh"
 #include "zpp_internal.h"
@@ -50,7 +49,7 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 constexpr int LN_VPT = 4;  // uint4 (8 bf16) vectors per thread
 
 // RMS = true: RMSNorm (LLaMA): mean fixed at 0, no beta; mean_out may be null.
-template <bool RMS, int NT, int VPT = LN_VPT>
+template <bool RMS, int NT>
 __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
                                                             const bf16* __restrict__ b, bf16* __restrict__ y,
                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
@@ -59,10 +58,10 @@ __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restric
   const int row = blockIdx.x;
   const bf16* xr = x + (long long)row * cols;
   const int nvec = cols / 8;
-  float v[VPT][8];
+  float v[LN_VPT][8];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       unpack8(*reinterpret_cast<const uint4*>(xr + vi * 8), v[i]);
@@ -73,7 +72,7 @@ __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restric
   const float mean = RMS ? 0.f : block_sum<NT>(s, red) / cols;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
 #pragma unroll
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restric
   const float rstd = rsqrtf(block_sum<NT>(q, red) / cols + eps);
   bf16* yr = y + (long long)row * cols;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       float gg[8], bb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
@@ -103,7 +102,7 @@ __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restric
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
 // the two row sums fused into a single float2 block reduction.  RMS: mean = 0 and the
 // mean(dy*g) term drops (xhat = x * rstd).
-template <bool RMS, int NT, int VPT = LN_VPT>
+template <bool RMS, int NT>
 __global__ void __launch_bounds__(NT) layernorm_bwd_dx_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                                               const float* __restrict__ mean,
                                                               const float* __restrict__ rstd,
@@ -115,11 +114,11 @@ __global__ void __launch_bounds__(NT) layernorm_bwd_dx_kernel(const bf16* __rest
   const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
   const bf16* xr = x + (long long)row * cols;
   const bf16* dyr = dy + (long long)row * cols;
-  float xh[VPT][8], dg[VPT][8];
-  uint4 rv[VPT];  // residual-gradient vectors, loaded with x / dy (more bytes in flight)
+  float xh[LN_VPT][8], dg[LN_VPT][8];
+  uint4 rv[LN_VPT];  // residual-gradient vectors, loaded with x / dy (more bytes in flight)
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       float xv[8], dv[8], gv[8];
@@ -150,7 +149,7 @@ __global__ void __launch_bounds__(NT) layernorm_bwd_dx_kernel(const bf16* __rest
   const float m1 = RMS ? 0.f : t.x / cols, m2 = t.y / cols;
   bf16* dxr = dx + (long long)row * cols;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < LN_VPT; ++i) {
     const int vi = threadIdx.x + i * NT;
     if (vi < nvec) {
       float o[8];
@@ -569,9 +568,7 @@ static int grid_for(long long n, int per_block) {
 
 int kernels_preload() {
   cudaFuncAttributes fa;
-  const void* fns[] = {(const void*)layernorm_fwd_kernel<false, 64, 8>, (const void*)layernorm_bwd_dx_kernel<false, 64, 8>,
-                       (const void*)layernorm_fwd_kernel<true, 64, 8>, (const void*)layernorm_bwd_dx_kernel<true, 64, 8>,
-                       (const void*)layernorm_fwd_kernel<false, 128>, (const void*)layernorm_bwd_dx_kernel<false, 128>,
+  const void* fns[] = {(const void*)layernorm_fwd_kernel<false, 128>, (const void*)layernorm_bwd_dx_kernel<false, 128>,
                        (const void*)layernorm_fwd_kernel<true, 128>, (const void*)layernorm_bwd_dx_kernel<true, 128>,
                        (const void*)layernorm_fwd_kernel<false, 256>, (const void*)layernorm_bwd_dx_kernel<false, 256>,
                        (const void*)layernorm_fwd_kernel<true, 256>, (const void*)layernorm_bwd_dx_kernel<true, 256>,
@@ -594,16 +591,9 @@ using namespace zpp;
 #define STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
 // 128 threads per row when the row fits in 4 vectors per thread, else 256
-// ZPP_LN_NT=64 (experiment, off by default): 64 threads x 8 vectors per row of <= 4096
-static bool ln_nt64() {
-  static int v = -1;
-  if (v < 0) v = getenv("ZPP_LN_NT") && atoi(getenv("ZPP_LN_NT")) == 64;
-  return v == 1;
-}
-#define LN_DISPATCH(cols, KERNEL, RMSV, ...)                                                                  \
-  ((ln_nt64() && (cols) <= 64 * 8 * 8) ? (KERNEL<RMSV, 64, 8><<<rows, 64, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
-   : (cols) <= 128 * 8 * LN_VPT        ? (KERNEL<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
-                                       : (KERNEL<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
+#define LN_DISPATCH(cols, KERNEL, RMSV, ...)                                                 \
+  ((cols) <= 128 * 8 * LN_VPT ? (KERNEL<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
+                              : (KERNEL<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
 
 extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                                  int rows, int cols, float eps, uintptr_t stream) {
