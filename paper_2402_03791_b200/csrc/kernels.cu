@@ -234,8 +234,16 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
     const int k = idx / CR_COLS, c = idx % CR_COLS;
     const int col = strip * CR_COLS + c;
     if (col >= cols) continue;
+    // all split partials in flight at once (L2 latency once, not nsplit times), then summed
+    // in split order: same bits as a sequential loop
+    float v[CR_MAX_SPLIT];
+#pragma unroll
+    for (int sp = 0; sp < CR_MAX_SPLIT; ++sp)
+      v[sp] = sp < nsplit ? __ldcg(&ws[((long long)sp * NO + k) * ws_ld + col]) : 0.f;
     float sum = 0.f;
-    for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(&ws[((long long)sp * NO + k) * ws_ld + col]);
+#pragma unroll
+    for (int sp = 0; sp < CR_MAX_SPLIT; ++sp)
+      if (sp < nsplit) sum += v[sp];
     float* o = k == 0 ? out0 : out1;
     if (o) o[col] = accumulate ? o[col] + sum : sum;
   }
@@ -243,8 +251,14 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
 }
 
 static int colred_splits(int rows, int strips) {
+  static int waves = -1;  // target blocks = waves x SMs (ZPP_CR_WAVES, A/B experiments only)
+  if (waves < 0) {
+    const char* e = getenv("ZPP_CR_WAVES");
+    waves = e ? atoi(e) : 2;
+    if (waves < 1) waves = 2;
+  }
   int s = 1;
-  while (s < CR_MAX_SPLIT && strips * s < 2 * num_sms() && rows / (2 * s) >= 64) s *= 2;
+  while (s < CR_MAX_SPLIT && strips * s < waves * num_sms() && rows / (2 * s) >= 64) s *= 2;
   return s;
 }
 
