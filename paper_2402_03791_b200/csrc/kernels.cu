@@ -99,6 +99,156 @@ __global__ void __launch_bounds__(NT) layernorm_fwd_kernel(const bf16* __restric
   }
 }
 
+// Row data streamed past L1 (gamma/beta, read by every row, stay L1-resident).
+__device__ __forceinline__ uint4 ld_na(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Packed-row variants for NT = 128 (ZPP_LN_PK=1, A/B): the row is held as packed bf16
+// (16 registers instead of 32 floats) and unpacked at each use, so more rows fit per SM.
+// Same arithmetic in the same order as layernorm_fwd_kernel / layernorm_bwd_dx_kernel:
+// bit-identical outputs.
+template <bool RMS>
+__global__ void __launch_bounds__(128) layernorm_fwd_pk_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                               const bf16* __restrict__ b, bf16* __restrict__ y,
+                                                               float* __restrict__ mean_out,
+                                                               float* __restrict__ rstd_out, int cols, float eps) {
+  constexpr int NT = 128;
+  __shared__ float red[NT / 32];
+  const int row = blockIdx.x;
+  const bf16* xr = x + (long long)row * cols;
+  const int nvec = cols / 8;
+  uint4 raw[LN_VPT];
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) raw[i] = ld_na(xr + vi * 8);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    if (threadIdx.x + i * NT < nvec) {
+      float v[8];
+      unpack8(raw[i], v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
+  }
+  const float mean = RMS ? 0.f : block_sum<NT>(s, red) / cols;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    if (threadIdx.x + i * NT < nvec) {
+      float v[8];
+      unpack8(raw[i], v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { const float d = v[j] - mean; q += d * d; }
+    }
+  }
+  const float rstd = rsqrtf(block_sum<NT>(q, red) / cols + eps);
+  bf16* yr = y + (long long)row * cols;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) {
+      float v[8], gg[8], bb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
+      unpack8(raw[i], v);
+      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg);
+      if (!RMS) unpack8(*reinterpret_cast<const uint4*>(b + vi * 8), bb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[j] - mean) * rstd * gg[j] + bb[j];
+      *reinterpret_cast<uint4*>(yr + vi * 8) = pack8(o);
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (!RMS) mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+template <bool RMS>
+__global__ void __launch_bounds__(128) layernorm_bwd_dx_pk_kernel(const bf16* __restrict__ dy,
+                                                                  const bf16* __restrict__ x,
+                                                                  const float* __restrict__ mean,
+                                                                  const float* __restrict__ rstd,
+                                                                  const bf16* __restrict__ g,
+                                                                  const bf16* __restrict__ dres,
+                                                                  bf16* __restrict__ dx, int cols) {
+  constexpr int NT = 128;
+  __shared__ float2 red[NT / 32];
+  const int row = blockIdx.x;
+  const int nvec = cols / 8;
+  const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
+  const bf16* xr = x + (long long)row * cols;
+  const bf16* dyr = dy + (long long)row * cols;
+  uint4 xw[LN_VPT], dw[LN_VPT], rv[LN_VPT];
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) {
+      xw[i] = ld_na(xr + vi * 8);
+      dw[i] = ld_na(dyr + vi * 8);
+      if (dres) rv[i] = ld_na(dres + (long long)row * cols + vi * 8);
+    }
+  }
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) {
+      float xv[8], dv[8], gv[8];
+      unpack8(xw[i], xv);
+      unpack8(dw[i], dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xv[j] - mu) * rs, dg = dv[j] * gv[j];
+        s1 += dg;
+        s2 += dg * xh;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = make_float2(s1, s2);
+  __syncthreads();
+  float2 t = red[0];
+#pragma unroll
+  for (int i = 1; i < NT / 32; ++i) { t.x += red[i].x; t.y += red[i].y; }
+  const float m1 = RMS ? 0.f : t.x / cols, m2 = t.y / cols;
+  bf16* dxr = dx + (long long)row * cols;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int vi = threadIdx.x + i * NT;
+    if (vi < nvec) {
+      float xv[8], dv[8], gv[8], o[8];
+      unpack8(xw[i], xv);
+      unpack8(dw[i], dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xv[j] - mu) * rs, dg = dv[j] * gv[j];
+        o[j] = rs * (dg - m1 - xh * m2);
+      }
+      if (dres) {
+        float r[8];
+        unpack8(rv[i], r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] += r[j];
+      }
+      *reinterpret_cast<uint4*>(dxr + vi * 8) = pack8(o);
+    }
+  }
+}
+
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
 // the two row sums fused into a single float2 block reduction.  RMS: mean = 0 and the
 // mean(dy*g) term drops (xhat = x * rstd).
@@ -586,6 +736,8 @@ int kernels_preload() {
                        (const void*)layernorm_fwd_kernel<true, 128>, (const void*)layernorm_bwd_dx_kernel<true, 128>,
                        (const void*)layernorm_fwd_kernel<false, 256>, (const void*)layernorm_bwd_dx_kernel<false, 256>,
                        (const void*)layernorm_fwd_kernel<true, 256>, (const void*)layernorm_bwd_dx_kernel<true, 256>,
+                       (const void*)layernorm_fwd_pk_kernel<false>, (const void*)layernorm_bwd_dx_pk_kernel<false>,
+                       (const void*)layernorm_fwd_pk_kernel<true>, (const void*)layernorm_bwd_dx_pk_kernel<true>,
                        (const void*)swiglu_fwd_kernel, (const void*)swiglu_bwd_kernel, (const void*)rope_kernel,
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_wte_kernel, (const void*)embed_bwd_wpe_kernel,
@@ -605,15 +757,23 @@ using namespace zpp;
 #define STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
 // 128 threads per row when the row fits in 4 vectors per thread, else 256
+// ZPP_LN_PK=1: packed-row 128-thread variants (A/B experiment)
+static bool ln_pk() {
+  static int v = -1;
+  if (v < 0) v = getenv("ZPP_LN_PK") && atoi(getenv("ZPP_LN_PK")) ? 1 : 0;
+  return v == 1;
+}
 #define LN_DISPATCH(cols, KERNEL, RMSV, ...)                                                 \
-  ((cols) <= 128 * 8 * LN_VPT ? (KERNEL<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
-                              : (KERNEL<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
+  ((cols) <= 128 * 8 * LN_VPT                                                                \
+       ? (ln_pk() ? (KERNEL##_pk_kernel<RMSV><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
+                  : (KERNEL##_kernel<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0)) \
+       : (KERNEL##_kernel<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
 
 extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_fwd_kernel, false, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean,
+  LN_DISPATCH(cols, layernorm_fwd, false, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean,
               rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
@@ -647,7 +807,7 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_bwd_dx_kernel, false, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
+  LN_DISPATCH(cols, layernorm_bwd_dx, false, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
               (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc || !dgamma) return rc;  // dgamma == null: parameter grads via zpp_norm_param_grads
@@ -659,7 +819,7 @@ extern "C" int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float*
                                uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_fwd_kernel, true, (const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y, nullptr, rstd,
+  LN_DISPATCH(cols, layernorm_fwd, true, (const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y, nullptr, rstd,
               cols, eps);
   return check_launch("rmsnorm_fwd");
 }
@@ -670,7 +830,7 @@ extern "C" int zpp_rmsnorm_bwd(const void* dy, const void* x, const float* rstd,
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_bwd_dx_kernel, true, (const bf16*)dy, (const bf16*)x, nullptr, rstd, (const bf16*)gamma,
+  LN_DISPATCH(cols, layernorm_bwd_dx, true, (const bf16*)dy, (const bf16*)x, nullptr, rstd, (const bf16*)gamma,
               (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("rmsnorm_bwd_dx");
   if (rc || !dgamma) return rc;
