@@ -108,68 +108,11 @@ __device__ __forceinline__ uint4 ld_na(const void* p) {
   return r;
 }
 
-// Packed-row variants for NT = 128 (ZPP_LN_PK=1, A/B): the row is held as packed bf16
-// (16 registers instead of 32 floats) and unpacked at each use, so more rows fit per SM.
-// Same arithmetic in the same order as layernorm_fwd_kernel / layernorm_bwd_dx_kernel:
-// bit-identical outputs.
-template <bool RMS>
-__global__ void __launch_bounds__(128) layernorm_fwd_pk_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
-                                                               const bf16* __restrict__ b, bf16* __restrict__ y,
-                                                               float* __restrict__ mean_out,
-                                                               float* __restrict__ rstd_out, int cols, float eps) {
-  constexpr int NT = 128;
-  __shared__ float red[NT / 32];
-  const int row = blockIdx.x;
-  const bf16* xr = x + (long long)row * cols;
-  const int nvec = cols / 8;
-  uint4 raw[LN_VPT];
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * NT;
-    if (vi < nvec) raw[i] = ld_na(xr + vi * 8);
-  }
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    if (threadIdx.x + i * NT < nvec) {
-      float v[8];
-      unpack8(raw[i], v);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) s += v[j];
-    }
-  }
-  const float mean = RMS ? 0.f : block_sum<NT>(s, red) / cols;
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    if (threadIdx.x + i * NT < nvec) {
-      float v[8];
-      unpack8(raw[i], v);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { const float d = v[j] - mean; q += d * d; }
-    }
-  }
-  const float rstd = rsqrtf(block_sum<NT>(q, red) / cols + eps);
-  bf16* yr = y + (long long)row * cols;
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * NT;
-    if (vi < nvec) {
-      float v[8], gg[8], bb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
-      unpack8(raw[i], v);
-      unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gg);
-      if (!RMS) unpack8(*reinterpret_cast<const uint4*>(b + vi * 8), bb);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = (v[j] - mean) * rstd * gg[j] + bb[j];
-      *reinterpret_cast<uint4*>(yr + vi * 8) = pack8(o);
-    }
-  }
-  if (threadIdx.x == 0) {
-    if (!RMS) mean_out[row] = mean;
-    rstd_out[row] = rstd;
-  }
-}
-
+// Backward dx for rows of <= 4096 columns (the default there): x, dy and the residual grad
+// are held as packed bf16 (48 registers instead of 64 floats + 16) and xhat, dy*g are
+// recomputed at each use, so 8 rows fit per SM instead of 5: 42.3 -> 34.6 us at 4096 x 4096
+// (profiles/r01d_ln_pk_ab.txt).  The same packing in the forward was slower (24.2 -> 26.1 us)
+// and is not used.
 template <bool RMS>
 __global__ void __launch_bounds__(128) layernorm_bwd_dx_pk_kernel(const bf16* __restrict__ dy,
                                                                   const bf16* __restrict__ x,
@@ -736,8 +679,7 @@ int kernels_preload() {
                        (const void*)layernorm_fwd_kernel<true, 128>, (const void*)layernorm_bwd_dx_kernel<true, 128>,
                        (const void*)layernorm_fwd_kernel<false, 256>, (const void*)layernorm_bwd_dx_kernel<false, 256>,
                        (const void*)layernorm_fwd_kernel<true, 256>, (const void*)layernorm_bwd_dx_kernel<true, 256>,
-                       (const void*)layernorm_fwd_pk_kernel<false>, (const void*)layernorm_bwd_dx_pk_kernel<false>,
-                       (const void*)layernorm_fwd_pk_kernel<true>, (const void*)layernorm_bwd_dx_pk_kernel<true>,
+                       (const void*)layernorm_bwd_dx_pk_kernel<false>, (const void*)layernorm_bwd_dx_pk_kernel<true>,
                        (const void*)swiglu_fwd_kernel, (const void*)swiglu_bwd_kernel, (const void*)rope_kernel,
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_wte_kernel, (const void*)embed_bwd_wpe_kernel,
@@ -757,23 +699,19 @@ using namespace zpp;
 #define STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
 // 128 threads per row when the row fits in 4 vectors per thread, else 256
-// ZPP_LN_PK=1: packed-row 128-thread variants (A/B experiment)
-static bool ln_pk() {
-  static int v = -1;
-  if (v < 0) v = getenv("ZPP_LN_PK") && atoi(getenv("ZPP_LN_PK")) ? 1 : 0;
-  return v == 1;
-}
 #define LN_DISPATCH(cols, KERNEL, RMSV, ...)                                                 \
-  ((cols) <= 128 * 8 * LN_VPT                                                                \
-       ? (ln_pk() ? (KERNEL##_pk_kernel<RMSV><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
-                  : (KERNEL##_kernel<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0)) \
-       : (KERNEL##_kernel<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
+  ((cols) <= 128 * 8 * LN_VPT ? (KERNEL<RMSV, 128><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0) \
+                              : (KERNEL<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
+#define LN_BWD_DISPATCH(cols, RMSV, ...)                                                                       \
+  ((cols) <= 128 * 8 * LN_VPT                                                                                  \
+       ? (layernorm_bwd_dx_pk_kernel<RMSV><<<rows, 128, 0, STREAM(stream)>>>(__VA_ARGS__), 0)                  \
+       : (layernorm_bwd_dx_kernel<RMSV, 256><<<rows, 256, 0, STREAM(stream)>>>(__VA_ARGS__), 0))
 
 extern "C" int zpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                                  int rows, int cols, float eps, uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_fwd, false, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean,
+  LN_DISPATCH(cols, layernorm_fwd_kernel, false, (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean,
               rstd, cols, eps);
   return check_launch("layernorm_fwd");
 }
@@ -807,7 +745,7 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "layernorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "layernorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_bwd_dx, false, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
+  LN_BWD_DISPATCH(cols, false, (const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)gamma,
               (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("layernorm_bwd_dx");
   if (rc || !dgamma) return rc;  // dgamma == null: parameter grads via zpp_norm_param_grads
@@ -819,7 +757,7 @@ extern "C" int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float*
                                uintptr_t stream) {
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm: cols % 8 != 0 or cols > 8192");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_fwd, true, (const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y, nullptr, rstd,
+  LN_DISPATCH(cols, layernorm_fwd_kernel, true, (const bf16*)x, (const bf16*)gamma, nullptr, (bf16*)y, nullptr, rstd,
               cols, eps);
   return check_launch("rmsnorm_fwd");
 }
@@ -830,7 +768,7 @@ extern "C" int zpp_rmsnorm_bwd(const void* dy, const void* x, const float* rstd,
   if (cols % 8 || cols > 256 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: cols % 8 != 0 or > 8192");
   if (!workspace && dgamma) return set_error(ZPP_ERR_ARG, "rmsnorm_bwd: workspace required");
   if (rows <= 0) return ZPP_OK;
-  LN_DISPATCH(cols, layernorm_bwd_dx, true, (const bf16*)dy, (const bf16*)x, nullptr, rstd, (const bf16*)gamma,
+  LN_BWD_DISPATCH(cols, true, (const bf16*)dy, (const bf16*)x, nullptr, rstd, (const bf16*)gamma,
               (const bf16*)dresid, (bf16*)dx, cols);
   int rc = check_launch("rmsnorm_bwd_dx");
   if (rc || !dgamma) return rc;
