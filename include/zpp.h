@@ -67,10 +67,9 @@ int zpp_gemm_set_streamk(int on);
 /* ---- causal multi-head attention, qkv packed [b, s, 3, heads, d] bf16 --------- */
 int zpp_attn_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, int head_dim,
                  uintptr_t stream);
-/* attention implementation policy: 0 = auto (tcgen05/TMEM kernels when seq % 128 == 0),
- * 1 = mma.sync FlashAttention-2 tiles (seq % 64 == 0).  Process-wide. */
-int zpp_attn_set_impl(int impl);
-/* workspace: batch*heads*seq floats (row-wise dO.O) + batch*seq*heads*head_dim floats (dQ accum) */
+/* seq % 128 == 0, head_dim 64 or 128.  Backward = dQ kernel (which also writes delta = rowsum(O*dO)
+ * and lse*log2(e) into the workspace) then the dK/dV kernel; deterministic (no atomics).
+ * workspace: 2*batch*heads*seq floats (delta | lse*log2e), 16-byte aligned */
 int zpp_attn_bwd(const void* qkv, const void* out, const float* lse, const void* dout, void* dqkv,
                  float* workspace, int batch, int seq, int heads, int head_dim, uintptr_t stream);
 long long zpp_attn_bwd_workspace_floats(int batch, int seq, int heads, int head_dim);

@@ -40,8 +40,8 @@ def gpt_forward_loss(params: dict, ids: torch.Tensor, labels: torch.Tensor, *, l
     wte, wpe = params[("wte", None)], params[("wpe", None)]
     h = wte.shape[1]
     dh = h // heads
-    x = wte[ids] + wpe[torch.arange(s)][None]
-    mask = torch.ones(s, s, dtype=torch.bool).triu(1)
+    x = wte[ids] + wpe[torch.arange(s, device=ids.device)][None]
+    mask = torch.ones(s, s, dtype=torch.bool, device=ids.device).triu(1)
     for l in range(layers):
         p = lambda n: params[(n, l)]  # noqa: E731
         xn = F.layer_norm(x, (h,), p("ln1_g"), p("ln1_b"), eps)
@@ -67,8 +67,8 @@ def _rms(x, g, eps):
 def _rope(t, base: float):
     """Rotate-half RoPE of t [N, H, s, d] at positions 0..s-1."""
     s, d = t.shape[-2], t.shape[-1]
-    inv = torch.exp2(-(2.0 * torch.arange(d // 2, dtype=torch.float32) / d) * math.log2(base))
-    ang = torch.arange(s, dtype=torch.float32)[:, None] * inv[None]
+    inv = torch.exp2(-(2.0 * torch.arange(d // 2, dtype=torch.float32, device=t.device) / d) * math.log2(base))
+    ang = torch.arange(s, dtype=torch.float32, device=t.device)[:, None] * inv[None]
     cos, sin = ang.cos(), ang.sin()
     a, b = t[..., : d // 2], t[..., d // 2:]
     return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
@@ -83,7 +83,7 @@ def llama_forward_loss(params: dict, ids: torch.Tensor, labels: torch.Tensor, *,
     h = wte.shape[1]
     dh = h // heads
     x = wte[ids]
-    mask = torch.ones(s, s, dtype=torch.bool).triu(1)
+    mask = torch.ones(s, s, dtype=torch.bool, device=ids.device).triu(1)
     for l in range(layers):
         p = lambda n: params[(n, l)]  # noqa: E731
         qkv = _rms(x, p("ln1_g"), eps) @ p("w_qkv").t()

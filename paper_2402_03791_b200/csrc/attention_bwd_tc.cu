@@ -1,22 +1,30 @@
-// Causal flash-attention BACKWARD on tcgen05, split into two kernels so that no partial
-// dQ ever leaves the SM (the fused key-outer kernel in attention_tc.cu reduce-adds a
-// 128x128 fp32 dQ partial per (key block, query block) pair through L2 -- 64 KB per pair
-// -- and that reduction, not the tensor core, set its pace).
+// Causal flash-attention BACKWARD on tcgen05 — two deterministic kernels, fully double-buffered
+// in TMEM by working on 64-wide tiles of the loop dimension.
 //
-//   attn_bwd_dkdv_tc_kernel  one CTA per (128-key block j, batch*head), loop over query
-//                            blocks i >= j:  S^T = K Q_i^T, dP^T = V dO_i^T,
-//                            dV += P^T dO_i (A = P^T from TMEM), dK += dS^T Q_i (A = dS^T smem)
-//   attn_bwd_dq_tc_kernel    one CTA per (128-query block i, batch*head), loop over key
-//                            blocks j <= i:  S = Q K_j^T, dP = dO V_j^T,
-//                            dQ += dS K_j (A = dS from TMEM, written over S)
+//   attn_bwd_dq_kernel    (launched first) one CTA per (128-query block i, b*h).
+//       Prologue: delta_i = rowsum(O_i * dO_i) (fp32, fixed order) and lse2 = lse*log2(e) for
+//       its 128 rows, both written to the workspace for the dK/dV kernel -- this replaces the
+//       separate delta pass (one read of O, and dO is already in smem).
+//       Loop over 64-key tiles j (keys <= last query):
+//         S_j = Q K_j^T, dP_j = dO V_j^T                (M=128 queries, N=64 keys)
+//         dS  = exp2(S*scale*log2e - lse2) (dP - delta) * scale   -> bf16 over S_j in TMEM
+//         dQ += dS K_j                                    (A = dS from TMEM, M=128, N=d)
+//   attn_bwd_dkdv_kernel  one CTA per (128-key block, b*h), loop over 64-query tiles:
+//         S^T = K Q^T, dP^T = V dO^T                      (M=128 keys, N=64 queries)
+//         P^T -> bf16 over S^T in TMEM, dS^T -> smem (128B-swizzled, K-major)
+//         dV += P^T dO (A from TMEM), dK += dS^T Q        (M=128 keys, N=d)
 //
-// The dQ kernel recomputes S and dP (2 of its 3 MMAs), i.e. 7 MMAs per (i, j) pair instead
-// of 5, but both kernels now keep the tensor pipe fed: every MMA that a softmax phase does
-// not depend on is issued ahead of it.
+// Why 64-wide tiles: with d = 128 the two 128x128 fp32 accumulators (dK, dV) take 256 of the
+// 512 TMEM columns.  A 64-query S^T / dP^T pair is 128 columns, so BOTH can be double
+// buffered: the softmax of tile t+1 runs while the tensor core executes dV(t), dK(t),
+// S^T(t+2), dP^T(t+2) -- the pipe never waits for the exp2 phase.  Same in the dQ kernel
+// (S and dP double-buffered, 256 columns, + dQ).
+// No partial gradient leaves the SM and there are no atomics: every output is a fixed-order
+// fp32 sum, so the backward is bit-reproducible run to run.
 //
-// Shared conventions (as attention_tc.cu): qkv [B*T, 3*H*D] bf16, dout [B*T, H*D],
-// lse [B, H, T] natural log, delta [B, H, T] = rowsum(O * dO); dqkv [B*T, 3*H*D] bf16.
-// 128B-swizzled [128 rows][64 cols] bf16 smem atoms loaded by 2-D TMA boxes {64, 128}.
+// Conventions: qkv [B*T, 3*H*D] bf16, out/dout [B*T, H*D], lse [B, H, T] natural log;
+// workspace = delta [B*H*T] | lse2 [B*H*T] fp32; dqkv [B*T, 3*H*D] bf16.  T % 128 == 0.
+// smem tiles are [rows][64 bf16] 128B-swizzled atoms loaded by 2-D TMA boxes {64, rows}.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -30,67 +38,399 @@ namespace zpp {
 
 typedef __nv_bfloat16 bf16;
 
+#ifdef ZPP_TRACE
+// Debug build only (make trace): clock64 stamps of CTA 0, [kernel][slot][tile], read by tools/attn_trace.py
+__device__ unsigned long long g_attn_trace[2][8][64];
+#define ZTRACE(k, slot, t) \
+  do {                     \
+    if (blockIdx.x == 0 && (t) < 64) g_attn_trace[k][slot][t] = clock64(); \
+  } while (0)
+#else
+#define ZTRACE(k, slot, t) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace {
 constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float dot8(uint4 a, uint4 b) {
+  float s = bf16lo(a.x) * bf16lo(b.x);
+  s = fmaf(bf16hi(a.x), bf16hi(b.x), s);
+  s = fmaf(bf16lo(a.y), bf16lo(b.y), s);
+  s = fmaf(bf16hi(a.y), bf16hi(b.y), s);
+  s = fmaf(bf16lo(a.z), bf16lo(b.z), s);
+  s = fmaf(bf16hi(a.z), bf16hi(b.z), s);
+  s = fmaf(bf16lo(a.w), bf16lo(b.w), s);
+  return fmaf(bf16hi(a.w), bf16hi(b.w), s);
 }
 
-// ---------------------------------------------------------------------------------------
-// dK / dV.  warp 0: TMA (K_j, V_j once; Q_i / dO_i ring of 2), warp 1: MMA issuer,
-// warp 2: TMEM owner, warps 4..11: softmax-bwd (warp (q, hh) = TMEM lane quarter q,
-// query-column half hh; thread = key row).
-// TMEM: dV [0,128) dK [128,256) S^T / P^T [256,384) dP^T [384,512).
-// MMA order per query block i (after ds_full(i)):  dV(i), S^T(i+1), dP^T(i+1), dK(i)
-// -> the softmax of block i+1 starts after three MMAs while dK(i) still runs.
+// Thread = TMEM lane r of a 128-row accumulator, half hh of its D columns -> bf16 row segment.
 template <int D>
-struct DkdvCfg {
-  static constexpr int ATOM = 128 * 128;
-  static constexpr int TILE = (D / 64) * ATOM;
-  static constexpr int K_OFF = 0;
-  static constexpr int V_OFF = K_OFF + TILE;
-  static constexpr int Q_OFF = V_OFF + TILE;        // 2 stages
-  static constexpr int DO_OFF = Q_OFF + 2 * TILE;   // 2 stages
-  static constexpr int DS_OFF = DO_OFF + 2 * TILE;  // dS^T: 2 atoms (128 keys x 128 queries)
-  static constexpr int L_OFF = DS_OFF + 2 * ATOM;   // lse*log2e [128], delta [128]
-  static constexpr int BAR_OFF = L_OFF + 1024;
-  static constexpr int SMEM = BAR_OFF + 128 + 1024;
+__device__ __forceinline__ void store_acc_row(uint32_t tacc, uint32_t lo, int hh, bf16* dst) {
+#pragma unroll 1
+  for (int c = hh * (D / 64); c < (hh + 1) * (D / 64); ++c) {
+    uint32_t v[32];
+    tmem_ld32(tacc + lo + c * 32, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8)
+      *reinterpret_cast<uint4*>(dst + c * 32 + k) =
+          make_uint4(pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                     pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
+                     pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
+                     pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
+  }
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// dQ (+ delta, lse2).  warp 0: TMA Q, dO once, K_j ring of 5 (K_j is read by S_j and dQ_j);
+// warp 3: TMA V_j ring of 4; warp 1: MMA issuer; warp 2: TMEM owner; warps 4..11: thread =
+// query row (TMEM lane), warp (quarter q, half hh) takes keys [32hh, 32hh+32) of each tile.
+// TMEM: S/dS [0,128) (2 x 64), dP [128,256) (2 x 64), dQ [256, 256+D).
+template <int D>
+struct BwdDqCfg {
+  static constexpr int QATOM = 128 * 128;  // [128 rows][64 bf16]
+  static constexpr int QTILE = (D / 64) * QATOM;
+  static constexpr int KATOM = 64 * 128;   // [64 rows][64 bf16]
+  static constexpr int KTILE = (D / 64) * KATOM;
+  // deep K / V rings: the load of K_{j+KST} can only start when dQ(j) retires, and at the
+  // tensor core's rate one 64-key tile takes ~0.5 us -- an L2 TMA round trip is about as long
+  static constexpr int KST = 5, VST = 4;
+  static constexpr int Q_OFF = 0;
+  static constexpr int DO_OFF = Q_OFF + QTILE;
+  static constexpr int K_OFF = DO_OFF + QTILE;
+  static constexpr int V_OFF = K_OFF + KST * KTILE;
+  static constexpr int RED_OFF = V_OFF + VST * KTILE;  // float [2][128] delta halves
+  static constexpr int BAR_OFF = RED_OFF + 1024;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "smem budget");
 };
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                            const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
-                            int T, int H, float scale) {
-  using C = DkdvCfg<D>;
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
+                       const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ out,
+                       const float* __restrict__ lse, float* __restrict__ delta_out, float* __restrict__ lse2_out,
+                       bf16* __restrict__ dqkv, int T, int H, int BH, float scale) {
+  using C = BwdDqCfg<D>;
   constexpr int NA = D / 64;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  float* sL = reinterpret_cast<float*>(gbase + C::L_OFF);
-  float* sDl = sL + 128;
+  float* red = reinterpret_cast<float*>(gbase + C::RED_OFF);
   const uint32_t bars = base + C::BAR_OFF;
-  const uint32_t kv_full = bars, qd_full0 = bars + 8, qd_empty0 = bars + 24, sp_full = bars + 40;
-  const uint32_t ds_full = bars + 48, ds_free = bars + 56, mm_done = bars + 64;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 96);
+  const uint32_t qd_full = bars, k_full0 = bars + 8, k_empty0 = k_full0 + 8 * C::KST;
+  const uint32_t v_full0 = k_empty0 + 8 * C::KST, v_empty0 = v_full0 + 8 * C::VST;
+  const uint32_t s_full0 = v_empty0 + 8 * C::VST, dp_full0 = s_full0 + 16, ds_full0 = dp_full0 + 16;
+  const uint32_t dq_done = ds_full0 + 16, qt_full = dq_done + 8;
+  static_assert(8 * (1 + 2 * C::KST + 2 * C::VST + 8) <= 240, "barrier area");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int kblk = blockIdx.x;  // longest (most query blocks) first
-  const int k0 = kblk * 128;
-  const int nq = T / 128 - kblk;
+  if (threadIdx.x == 128) ZTRACE(0, 0, 63);
+  // 1-D grid, heaviest query blocks first across ALL heads
+  const int nqb = T / 128;
+  const int bh = blockIdx.x % BH, b = bh / H, h = bh % H;
+  const int qblk = nqb - 1 - static_cast<int>(blockIdx.x) / BH;
+  const int q0 = qblk * 128;
+  const int nkt = 2 * (qblk + 1);  // 64-key tiles up to the diagonal
   const int row_base = b * T;
 
   if (threadIdx.x == 0) {
-    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_kv);
+    tma_prefetch(&tm_do);
+    mbar_init(qd_full, 1);
+    for (int s = 0; s < C::KST; ++s) {
+      mbar_init(k_full0 + 8 * s, 1);
+      mbar_init(k_empty0 + 8 * s, 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
+      mbar_init(v_full0 + 8 * s, 1);
+      mbar_init(v_empty0 + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(s_full0 + 8 * s, 1);
+      mbar_init(dp_full0 + 8 * s, 1);
+      mbar_init(ds_full0 + 8 * s, 256);
+    }
+    mbar_init(dq_done, 1);
+    mbar_init(qt_full, 256);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // Q and dO live in TMEM as the A operands of S and dP (TS-mode MMAs: an SS MMA with N = 64
+  // is bound by the smem read of its 128-row A operand, 48 instead of 32 cycles per K16)
+  const uint32_t T_S = tmem, T_DP = tmem + 128, T_DQ = tmem + 256, T_Q = T_DQ + D, T_DO = T_Q + D / 2;
+  if (threadIdx.x == 128) ZTRACE(0, 1, 63);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qd_full, 2 * C::QTILE);
+      for (int a = 0; a < NA; ++a) {
+        tma_load_2d(base + C::Q_OFF + a * C::QATOM, &tm_q, qd_full, h * D + 64 * a, row_base + q0);
+        tma_load_2d(base + C::DO_OFF + a * C::QATOM, &tm_do, qd_full, h * D + 64 * a, row_base + q0);
+      }
+      for (int j = 0; j < nkt; ++j) {
+        const int st = j % C::KST;
+        mbar_wait(k_empty0 + 8 * st, ((j / C::KST) & 1) ^ 1);
+        const uint32_t fb = k_full0 + 8 * st;
+        mbar_arrive_expect_tx(fb, C::KTILE);
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(base + C::K_OFF + st * C::KTILE + a * C::KATOM, &tm_kv, fb, H * D + h * D + 64 * a,
+                      row_base + j * 64);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    if (lane == 0) {
+      for (int j = 0; j < nkt; ++j) {
+        const int st = j % C::VST;
+        mbar_wait(v_empty0 + 8 * st, ((j / C::VST) & 1) ^ 1);
+        const uint32_t fb = v_full0 + 8 * st;
+        mbar_arrive_expect_tx(fb, C::KTILE);
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(base + C::V_OFF + st * C::KTILE + a * C::KATOM, &tm_kv, fb, 2 * H * D + h * D + 64 * a,
+                      row_base + j * 64);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    {  // whole warp: uniform descriptors, elect.sync issues
+      constexpr uint32_t id_s = make_idesc_bf16(128, 64, false, false);  // S, dP: N = 64 keys
+      constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);    // dQ: B = K_j N-major (N = d)
+      auto issue_s = [&](int j) {
+        const int st = j % C::KST;
+        mbar_wait(k_full0 + 8 * st, (j / C::KST) & 1);
+        tc_fence_after();
+        const uint32_t kb = base + C::K_OFF + st * C::KTILE;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_ts_w(T_S + (j & 1) * 64, T_Q + kk * 8,
+                        make_sdesc(kb + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+        mma_commit_w(s_full0 + 8 * (j & 1));
+      };
+      auto issue_dp = [&](int j) {
+        const int st = j % C::VST;
+        mbar_wait(v_full0 + 8 * st, (j / C::VST) & 1);
+        tc_fence_after();
+        const uint32_t vb = base + C::V_OFF + st * C::KTILE;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_ts_w(T_DP + (j & 1) * 64, T_DO + kk * 8,
+                        make_sdesc(vb + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+        mma_commit_w(dp_full0 + 8 * (j & 1));
+        mma_commit_w(v_empty0 + 8 * st);
+      };
+      mbar_wait(qt_full, 0);  // Q, dO copied into TMEM by the row threads
+      tc_fence_after();
+      issue_s(0);
+      issue_dp(0);
+      if (nkt > 1) {
+        issue_s(1);
+        issue_dp(1);
+      }
+      for (int j = 0; j < nkt; ++j) {
+        ZTRACE(0, 0, j);
+        mbar_wait(ds_full0 + 8 * (j & 1), (j >> 1) & 1);
+        ZTRACE(0, 1, j);
+        tc_fence_after();
+        const uint32_t kb = base + C::K_OFF + (j % C::KST) * C::KTILE;
+        // dQ += dS K_j: A = dS in TMEM (each 32-key half packed into its first 16 columns)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16_ts_w(T_DQ, T_S + (j & 1) * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                      make_sdesc(kb + kk * 2048, C::KATOM, 1024), id_q, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(k_empty0 + 8 * (j % C::KST));
+        if (j + 2 < nkt) {  // buffers (j & 1): dS_j read by the dQ MMA above (in-order pipe)
+          issue_s(j + 2);
+          ZTRACE(0, 2, j);
+          issue_dp(j + 2);
+        }
+        ZTRACE(0, 3, j);
+      }
+      mma_commit_w(dq_done);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int hh = (warp - 4) >> 2;
+    const int r = q * 32 + lane;  // query row == TMEM lane
+    const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
+    const float sl2 = scale * kLog2e;
+    const float lse2_r = lse[(long long)bh * T + q0 + r] * kLog2e;
+    // delta = rowsum(O * dO): this thread sums half hh of the row's D columns (O from global,
+    // read once here; dO from the swizzled smem tile)
+    constexpr int CH = D / 16;  // 16-byte chunks per half row
+    uint4 ov[CH];
+    const uint4* orow = reinterpret_cast<const uint4*>(out + ((long long)row_base + q0 + r) * H * D + h * D) + hh * CH;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) ov[i] = __ldg(orow + i);
+    mbar_wait(qd_full, 0);
+    if (threadIdx.x == 128) ZTRACE(0, 2, 63);
+    float acc = 0.f;
+    {
+      // this thread's half row of Q and dO -> TMEM (lane r, packed bf16 pairs), and delta
+      uint32_t qv[4 * CH], dv[4 * CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int cg = hh * CH + i;  // global chunk index along D
+        const uint32_t off = (cg >> 3) * C::QATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
+        const uint4 d4 = ld_shared_v4(base + C::DO_OFF + off);
+        const uint4 q4 = ld_shared_v4(base + C::Q_OFF + off);
+        acc += dot8(ov[i], d4);
+        dv[4 * i] = d4.x, dv[4 * i + 1] = d4.y, dv[4 * i + 2] = d4.z, dv[4 * i + 3] = d4.w;
+        qv[4 * i] = q4.x, qv[4 * i + 1] = q4.y, qv[4 * i + 2] = q4.z, qv[4 * i + 3] = q4.w;
+      }
+      if constexpr (CH == 8) {
+        tmem_st32(T_Q + lo + hh * 32, qv);
+        tmem_st32(T_DO + lo + hh * 32, dv);
+      } else {
+        tmem_st16(T_Q + lo + hh * 16, qv);
+        tmem_st16(T_DO + lo + hh * 16, dv);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(qt_full);
+    }
+    red[hh * 128 + r] = acc;
+    named_bar_sync(1, 256);
+    const float delta_r = red[r] + red[128 + r];
+    if (hh == 0) {
+      delta_out[(long long)bh * T + q0 + r] = delta_r;
+      lse2_out[(long long)bh * T + q0 + r] = lse2_r;
+    }
+    for (int j = 0; j < nkt; ++j) {
+      const int buf = j & 1;
+      const uint32_t par = (j >> 1) & 1;
+      const uint32_t ts = T_S + lo + buf * 64 + hh * 32;
+#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (softmax warps only hand over)
+      mbar_wait(s_full0 + 8 * buf, par);
+      mbar_wait(dp_full0 + 8 * buf, par);
+      tc_fence_before();
+      mbar_arrive(ds_full0 + 8 * buf);
+      if (threadIdx.x == 128) ZTRACE(0, 7, j);
+      continue;
+#endif
+      if (threadIdx.x == 128) ZTRACE(0, 4, j);
+      mbar_wait(s_full0 + 8 * buf, par);
+      if (threadIdx.x == 128) ZTRACE(0, 5, j);
+      tc_fence_after();
+      float p[32];
+      {
+        uint32_t v[32];
+        tmem_ld32(ts, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) p[k] = fast_exp2(fmaf(__uint_as_float(v[k]), sl2, -lse2_r));
+      }
+      if (j >= nkt - 2) {  // the two tiles that straddle the diagonal: keys after the query
+        const int kq = j * 64 + hh * 32 - q0 - r;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (kq + k > 0) p[k] = 0.f;
+      }
+      if (threadIdx.x == 128) ZTRACE(0, 6, j);
+      mbar_wait(dp_full0 + 8 * buf, par);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(T_DP + lo + buf * 64 + hh * 32, v);
+      tmem_wait_ld();
+      uint32_t pk[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        pk[k] = pack_bf16(p[2 * k] * (__uint_as_float(v[2 * k]) - delta_r) * scale,
+                          p[2 * k + 1] * (__uint_as_float(v[2 * k + 1]) - delta_r) * scale);
+      tmem_st16(ts, pk);  // over S columns this warp has already read
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full0 + 8 * buf);
+      if (threadIdx.x == 128) ZTRACE(0, 7, j);
+    }
+    mbar_wait(dq_done, 0);
+    if (threadIdx.x == 128) ZTRACE(0, 4, 63);
+    tc_fence_after();
+    store_acc_row<D>(T_DQ, lo, hh, dqkv + ((long long)row_base + q0 + r) * 3 * H * D + (long long)h * D);
+    if (threadIdx.x == 128) ZTRACE(0, 5, 63);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------------------
+// dK / dV.  warp 0: TMA K, V once, then Q_t / dO_t (+ lse2_t, delta_t) through a ring of 4;
+// warp 1: MMA issuer; warp 2: TMEM owner; warps 4..11: thread = key row (TMEM lane), warp
+// (quarter q, half hh) takes queries [32hh, 32hh+32) of each 64-query tile.
+// TMEM: dV [0,D), dK [D,2D), S^T/P^T [2D,2D+128) (2 x 64), dP^T [2D+128, 2D+256) (2 x 64).
+template <int D>
+struct BwdDkdvCfg {
+  static constexpr int KATOM = 128 * 128;  // [128 rows][64 bf16]
+  static constexpr int KTILE = (D / 64) * KATOM;
+  static constexpr int QATOM = 64 * 128;   // [64 rows][64 bf16]
+  static constexpr int QTILE = (D / 64) * QATOM;
+  // ring of 4: the Q/dO stage of tile t+4 frees when dK(t) retires, two tiles before S^T(t+4)
+  // is issued -- one tile (~0.5 us at the tensor core's rate) does not hide an L2 TMA round trip
+  static constexpr int QST = 4;
+  static constexpr int DS_BYTES = 128 * 128;  // dS^T [128 keys][64 queries] bf16 (one buffer)
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + KTILE;
+  static constexpr int Q_OFF = V_OFF + KTILE;
+  static constexpr int DO_OFF = Q_OFF + QST * QTILE;
+  static constexpr int DS_OFF = DO_OFF + QST * QTILE;
+  static constexpr int L_OFF = DS_OFF + DS_BYTES;  // per stage: lse2 [64] | delta [64]
+  static constexpr int BAR_OFF = L_OFF + QST * 512;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static_assert(SMEM <= 232448, "smem budget");
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse2,
+                         const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, int BH,
+                         float scale) {
+  using C = BwdDkdvCfg<D>;
+  constexpr int NA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t bars = base + C::BAR_OFF;
+  const uint32_t kv_full = bars, qd_full0 = bars + 8, qd_empty0 = qd_full0 + 8 * C::QST;
+  const uint32_t sp_full0 = qd_empty0 + 8 * C::QST, ds_full0 = sp_full0 + 16, ds_free = ds_full0 + 16;
+  const uint32_t mm_done = ds_free + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 128) ZTRACE(1, 0, 63);
+  const int bh = blockIdx.x % BH, b = bh / H, h = bh % H;
+  const int kblk = static_cast<int>(blockIdx.x) / BH;  // block 0 has the most query tiles: first
+  const int k0 = kblk * 128;
+  const int nq = 2 * (T / 128 - kblk);  // 64-query tiles from the diagonal on
+  const int row_base = b * T;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_kv);
+    tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::QST; ++s) {
       mbar_init(qd_full0 + 8 * s, 1);
       mbar_init(qd_empty0 + 8 * s, 1);
     }
-    mbar_init(sp_full, 1);
-    mbar_init(ds_full, 256);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(sp_full0 + 8 * s, 1);
+      mbar_init(ds_full0 + 8 * s, 256);
+    }
     mbar_init(ds_free, 1);
     mbar_init(mm_done, 1);
     fence_mbar_init();
@@ -100,156 +440,143 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t T_DV = tmem, T_DK = tmem + 128, T_S = tmem + 256, T_DP = tmem + 384;
+  const uint32_t T_DV = tmem, T_DK = tmem + D, T_S = tmem + 2 * D, T_DP = tmem + 2 * D + 128;
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
+      mbar_arrive_expect_tx(kv_full, 2 * C::KTILE);
       for (int a = 0; a < NA; ++a) {
-        tma_load_2d(base + C::K_OFF + a * C::ATOM, &tm_qkv, kv_full, H * D + h * D + 64 * a, row_base + k0);
-        tma_load_2d(base + C::V_OFF + a * C::ATOM, &tm_qkv, kv_full, 2 * H * D + h * D + 64 * a, row_base + k0);
+        tma_load_2d(base + C::K_OFF + a * C::KATOM, &tm_kv, kv_full, H * D + h * D + 64 * a, row_base + k0);
+        tma_load_2d(base + C::V_OFF + a * C::KATOM, &tm_kv, kv_full, 2 * H * D + h * D + 64 * a, row_base + k0);
       }
       for (int it = 0; it < nq; ++it) {
-        const int st = it & 1;
-        const int q0 = (kblk + it) * 128;
-        mbar_wait(qd_empty0 + 8 * st, ((it >> 1) & 1) ^ 1);
+        const int st = it % C::QST;
+        const int q0 = k0 + it * 64;
+        mbar_wait(qd_empty0 + 8 * st, ((it / C::QST) & 1) ^ 1);
         const uint32_t fb = qd_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, 2 * C::TILE);
+        mbar_arrive_expect_tx(fb, 2 * C::QTILE + 512);
         for (int a = 0; a < NA; ++a) {
-          tma_load_2d(base + C::Q_OFF + st * C::TILE + a * C::ATOM, &tm_qkv, fb, h * D + 64 * a, row_base + q0);
-          tma_load_2d(base + C::DO_OFF + st * C::TILE + a * C::ATOM, &tm_do, fb, h * D + 64 * a, row_base + q0);
+          tma_load_2d(base + C::Q_OFF + st * C::QTILE + a * C::QATOM, &tm_q, fb, h * D + 64 * a, row_base + q0);
+          tma_load_2d(base + C::DO_OFF + st * C::QTILE + a * C::QATOM, &tm_do, fb, h * D + 64 * a, row_base + q0);
         }
+        bulk_load_1d(base + C::L_OFF + st * 512, lse2 + (long long)bh * T + q0, 256, fb);
+        bulk_load_1d(base + C::L_OFF + st * 512 + 256, delta + (long long)bh * T + q0, 256, fb);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T (N = 128 queries)
-      constexpr uint32_t id_kmn = make_idesc_bf16(128, D, false, true);    // dV, dK (B MN-major, N = d)
+    {  // whole warp: uniform descriptors, elect.sync issues
+      constexpr uint32_t id_sp = make_idesc_bf16(128, 64, false, false);  // S^T, dP^T: N = 64 queries
+      constexpr uint32_t id_kv = make_idesc_bf16(128, D, false, true);    // dV, dK: B N-major (N = d)
       mbar_wait(kv_full, 0);
-      auto issue_sp = [&](int it) {  // S^T = K Q^T and dP^T = V dO^T of query block it
-        const int st = it & 1;
-        mbar_wait(qd_full0 + 8 * st, (it >> 1) & 1);
+      auto issue_sp = [&](int it) {
+        const int st = it % C::QST;
+        mbar_wait(qd_full0 + 8 * st, (it / C::QST) & 1);
         tc_fence_after();
-        const uint32_t qs = base + C::Q_OFF + st * C::TILE, ds_ = base + C::DO_OFF + st * C::TILE;
+        const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+        const uint32_t buf = (it & 1) * 64;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::ATOM + (kk & 3) * 32;
-          mma_bf16(T_S, make_sdesc(base + C::K_OFF + off, 16, 1024), make_sdesc(qs + off, 16, 1024), id_kk,
-                   kk > 0 ? 1u : 0u);
-        }
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_w(T_S + buf, make_sdesc(base + C::K_OFF + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024),
+                   make_sdesc(qs + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024), id_sp, kk > 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::ATOM + (kk & 3) * 32;
-          mma_bf16(T_DP, make_sdesc(base + C::V_OFF + off, 16, 1024), make_sdesc(ds_ + off, 16, 1024), id_kk,
-                   kk > 0 ? 1u : 0u);
-        }
-        mma_commit(sp_full);
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_w(T_DP + buf, make_sdesc(base + C::V_OFF + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024),
+                   make_sdesc(dos + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024), id_sp, kk > 0 ? 1u : 0u);
+        mma_commit_w(sp_full0 + 8 * (it & 1));
       };
       issue_sp(0);
+      if (nq > 1) issue_sp(1);
       for (int it = 0; it < nq; ++it) {
-        const int st = it & 1;
-        const uint32_t qs = base + C::Q_OFF + st * C::TILE, ds_ = base + C::DO_OFF + st * C::TILE;
-        mbar_wait(ds_full, it & 1);
+        const int st = it % C::QST;
+        const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+        ZTRACE(1, 0, it);
+        mbar_wait(ds_full0 + 8 * (it & 1), (it >> 1) & 1);
+        ZTRACE(1, 1, it);
         tc_fence_after();
+        const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dV += P^T dO : A = P^T (TMEM, 8 packed columns per k16)
-          mma_bf16_ts(T_DV, T_S + (kk >> 2) * 64 + (kk & 3) * 8, make_sdesc(ds_ + kk * 2048, C::ATOM, 1024), id_kmn,
-                      (it > 0 || kk > 0) ? 1u : 0u);
-        if (it + 1 < nq) issue_sp(it + 1);  // S^T over P^T after dV read it (in-order pipe)
+        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO: A = P^T (TMEM, each 32-query half in its first 16 cols)
+          mma_bf16_ts_w(T_DV, T_S + (it & 1) * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                      make_sdesc(dos + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dK += dS^T Q : A = dS^T (smem K-major), B = Q (MN-major)
-          mma_bf16(T_DK, make_sdesc(base + C::DS_OFF + (kk >> 2) * C::ATOM + (kk & 3) * 32, 16, 1024),
-                   make_sdesc(qs + kk * 2048, C::ATOM, 1024), id_kmn, (it > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(ds_free);
-        mma_commit(qd_empty0 + 8 * st);
+        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q: A = dS^T (smem K-major), B = Q (N-major)
+          mma_bf16_w(T_DK, make_sdesc(base + C::DS_OFF + kk * 32, 16, 1024),
+                   make_sdesc(qs + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
+        mma_commit_w(ds_free);
+        mma_commit_w(qd_empty0 + 8 * st);
+        ZTRACE(1, 2, it);
+        if (it + 2 < nq) issue_sp(it + 2);  // S^T over P^T(it) after dV read it (in-order pipe)
+        ZTRACE(1, 3, it);
       }
-      mma_commit(mm_done);
+      mma_commit_w(mm_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int hh = (warp - 4) >> 2;
-    const int r = q * 32 + lane;  // key row
+    const int r = q * 32 + lane;  // key row == TMEM lane
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * kLog2e;
-    float nl = lse[(long long)bh * T + kblk * 128 + r] * kLog2e;
-    float nd = delta[(long long)bh * T + kblk * 128 + r];
     for (int it = 0; it < nq; ++it) {
-      const int q0 = (kblk + it) * 128;
-      named_bar_sync(1, 256);  // everyone is done reading the previous block's lse / delta
-      if (hh == 0) {
-        sL[r] = nl;
-        sDl[r] = nd;
-      }
-      named_bar_sync(1, 256);
-      if (it + 1 < nq) {
-        nl = lse[(long long)bh * T + q0 + 128 + r] * kLog2e;
-        nd = delta[(long long)bh * T + q0 + 128 + r];
-      }
-      mbar_wait(sp_full, it & 1);
+      const int buf = it & 1;
+      const uint32_t par = (it >> 1) & 1;
+      const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (it % C::QST) * 512) + hh * 32;
+      if (threadIdx.x == 128) ZTRACE(1, 4, it);
+      mbar_wait(sp_full0 + 8 * buf, par);
+      if (threadIdx.x == 128) ZTRACE(1, 5, it);
       tc_fence_after();
-      if (it > 0) mbar_wait(ds_free, (it - 1) & 1);  // dK(it-1) finished reading dS^T smem
-#pragma unroll 1
-      for (int c = 2 * hh; c < 2 * hh + 2; ++c) {  // 32 queries per chunk, this warp's half
-        uint32_t sv[32], pv[32];
-        tmem_ld32(T_S + lo + c * 32, sv);
-        tmem_ld32(T_DP + lo + c * 32, pv);
-        tmem_wait_ld();
-        float p[32], ds[32];
+      uint32_t sv[32], pv[32];
+      tmem_ld32(T_S + lo + buf * 64 + hh * 32, sv);
+      tmem_ld32(T_DP + lo + buf * 64 + hh * 32, pv);
+      tmem_wait_ld();
+      float p[32], ds[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int qi = c * 32 + j;
-          float pj = fast_exp2(__uint_as_float(sv[j]) * sl2 - sL[qi]);
-          if (it == 0 && r > qi) pj = 0.f;  // diagonal block: key after query
-          p[j] = pj;
-          ds[j] = pj * (__uint_as_float(pv[j]) - sDl[qi]) * scale;
+      for (int j = 0; j < 32; j += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(L + j);
+        const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + j);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          p[j + u] = fast_exp2(fmaf(__uint_as_float(sv[j + u]), sl2, -lv[u]));
+          ds[j + u] = dv[u];
         }
-        uint32_t pk[16];
+      }
+      if (it < 2) {  // tiles on the diagonal: key after query
+        const int qk = it * 64 + hh * 32 - r;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
-        // P^T bf16 over the S^T columns this warp already consumed (each column half packs into
-        // its own first 32 columns, so the other half's scores are never overwritten)
-        tmem_st16(T_S + lo + (c >> 1) * 64 + (c & 1) * 16, pk);
-        const uint32_t rowp = base + C::DS_OFF + (c >> 1) * C::ATOM + r * 128;
+        for (int j = 0; j < 32; ++j)
+          if (qk + j < 0) p[j] = 0.f;
+      }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int c8 = (c & 1) * 4 + t;
-          const float* s = &ds[t * 8];
-          st_shared_v4(rowp + ((c8 ^ (r & 7)) << 4), pack_bf16(s[0], s[1]), pack_bf16(s[2], s[3]),
-                       pack_bf16(s[4], s[5]), pack_bf16(s[6], s[7]));
-        }
+      for (int j = 0; j < 32; ++j) ds[j] = p[j] * (__uint_as_float(pv[j]) - ds[j]) * scale;
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
+      tmem_st16(T_S + lo + buf * 64 + hh * 32, pk);  // P^T over S^T columns this warp has read
+      if (threadIdx.x == 128) ZTRACE(1, 6, it);
+      if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);  // dK(it-1) done reading dS^T
+      const uint32_t rowp = base + C::DS_OFF + r * 128;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c8 = hh * 4 + t;
+        const float* s = &ds[t * 8];
+        st_shared_v4(rowp + ((c8 ^ (r & 7)) << 4), pack_bf16(s[0], s[1]), pack_bf16(s[2], s[3]),
+                     pack_bf16(s[4], s[5]), pack_bf16(s[6], s[7]));
       }
       tmem_wait_st();
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(ds_full);
+      mbar_arrive(ds_full0 + 8 * buf);
+      if (threadIdx.x == 128) ZTRACE(1, 7, it);
     }
-    // final dK / dV rows (thread = key row)
     mbar_wait(mm_done, 0);
+    if (threadIdx.x == 128) ZTRACE(1, 4, 63);
     tc_fence_after();
     bf16* dk = dqkv + ((long long)row_base + k0 + r) * 3 * H * D + (long long)H * D + (long long)h * D;
-    bf16* dv = dk + (long long)H * D;
-#pragma unroll 1
-    for (int c = hh * (D / 64); c < (hh + 1) * (D / 64); ++c) {
-      uint32_t a[32], bb[32];
-      tmem_ld32(T_DK + lo + c * 32, a);
-      tmem_ld32(T_DV + lo + c * 32, bb);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        *reinterpret_cast<uint4*>(dk + c * 32 + j) = make_uint4(
-            pack_bf16(__uint_as_float(a[j]), __uint_as_float(a[j + 1])),
-            pack_bf16(__uint_as_float(a[j + 2]), __uint_as_float(a[j + 3])),
-            pack_bf16(__uint_as_float(a[j + 4]), __uint_as_float(a[j + 5])),
-            pack_bf16(__uint_as_float(a[j + 6]), __uint_as_float(a[j + 7])));
-        *reinterpret_cast<uint4*>(dv + c * 32 + j) = make_uint4(
-            pack_bf16(__uint_as_float(bb[j]), __uint_as_float(bb[j + 1])),
-            pack_bf16(__uint_as_float(bb[j + 2]), __uint_as_float(bb[j + 3])),
-            pack_bf16(__uint_as_float(bb[j + 4]), __uint_as_float(bb[j + 5])),
-            pack_bf16(__uint_as_float(bb[j + 6]), __uint_as_float(bb[j + 7])));
-      }
-    }
+    store_acc_row<D>(T_DK, lo, hh, dk);
+    store_acc_row<D>(T_DV, lo, hh, dk + (long long)H * D);
+    if (threadIdx.x == 128) ZTRACE(1, 5, 63);
   }
   tc_fence_before();
   __syncthreads();
@@ -257,289 +584,76 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-// ---------------------------------------------------------------------------------------
-// dQ.  warp 0: TMA (Q_i, dO_i once; K_j ring of 3 -- K is read by S_j and dQ_j), warp 3:
-// TMA V_j ring of 2, warp 1: MMA issuer, warp 2: TMEM owner, warps 4..11: thread = query
-// row, warp (q, hh) takes key-column half hh (2 softmax warps per SM sub-partition).
-// TMEM: S_j double buffer [0,256) (dS_j bf16: each 64-key half packed over the first 32 of
-// its own S columns), dP [256,384), dQ [384,512).
-// Per key block j the row threads compute P = exp2(S*scale*log2e - lse*log2e) as soon as
-// S_j lands, then wait for dP_j, form dS = P (dP - delta) * scale into TMEM and signal; the
-// MMA warp then issues dP_{j+1} (dP's columns are free) and dQ += dS_j K_j, with S_{j+1}
-// already issued one block ahead.
-template <int D>
-struct DqCfg {
-  static constexpr int ATOM = 128 * 128;
-  static constexpr int TILE = (D / 64) * ATOM;
-  static constexpr int KST = 3;
-  static constexpr int Q_OFF = 0;
-  static constexpr int DO_OFF = Q_OFF + TILE;
-  static constexpr int K_OFF = DO_OFF + TILE;      // KST stages
-  static constexpr int V_OFF = K_OFF + KST * TILE;  // 2 stages
-  static constexpr int BAR_OFF = V_OFF + 2 * TILE;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static_assert(SMEM <= 232448, "smem budget");
-};
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                          const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
-                          int T, int H, float scale) {
-  using C = DqCfg<D>;
-  constexpr int NA = D / 64;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t bars = base + C::BAR_OFF;
-  const uint32_t qd_full = bars, k_full0 = bars + 8, k_empty0 = bars + 32, v_full0 = bars + 56;
-  const uint32_t v_empty0 = bars + 72, s_full0 = bars + 88, dp_full = bars + 104, ds_full = bars + 112;
-  const uint32_t dq_done = bars + 120;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 192);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int qblk = gridDim.x - 1 - blockIdx.x;  // longest (most key blocks) first
-  const int q0 = qblk * 128;
-  const int nkb = qblk + 1;
-  const int row_base = b * T;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch(&tm_qkv);
-    tma_prefetch(&tm_do);
-    mbar_init(qd_full, 1);
-    for (int s = 0; s < C::KST; ++s) {
-      mbar_init(k_full0 + 8 * s, 1);
-      mbar_init(k_empty0 + 8 * s, 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(v_full0 + 8 * s, 1);
-      mbar_init(v_empty0 + 8 * s, 1);
-      mbar_init(s_full0 + 8 * s, 1);
-    }
-    mbar_init(dp_full, 1);
-    mbar_init(ds_full, 256);
-    mbar_init(dq_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t T_S = tmem, T_DP = tmem + 256, T_DQ = tmem + 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(qd_full, 2 * C::TILE);
-      for (int a = 0; a < NA; ++a) {
-        tma_load_2d(base + C::Q_OFF + a * C::ATOM, &tm_qkv, qd_full, h * D + 64 * a, row_base + q0);
-        tma_load_2d(base + C::DO_OFF + a * C::ATOM, &tm_do, qd_full, h * D + 64 * a, row_base + q0);
-      }
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j % C::KST;
-        mbar_wait(k_empty0 + 8 * st, ((j / C::KST) & 1) ^ 1);
-        const uint32_t fb = k_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, C::TILE);
-        for (int a = 0; a < NA; ++a)
-          tma_load_2d(base + C::K_OFF + st * C::TILE + a * C::ATOM, &tm_qkv, fb, H * D + h * D + 64 * a,
-                      row_base + j * 128);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 3) {
-    if (lane == 0) {
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        mbar_wait(v_empty0 + 8 * st, ((j >> 1) & 1) ^ 1);
-        const uint32_t fb = v_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, C::TILE);
-        for (int a = 0; a < NA; ++a)
-          tma_load_2d(base + C::V_OFF + st * C::TILE + a * C::ATOM, &tm_qkv, fb, 2 * H * D + h * D + 64 * a,
-                      row_base + j * 128);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = make_idesc_bf16(128, 128, false, false);  // S, dP (N = 128 keys)
-      constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);     // dQ (B = K MN-major, N = d)
-      auto issue_s = [&](int j) {
-        const int st = j % C::KST;
-        mbar_wait(k_full0 + 8 * st, (j / C::KST) & 1);
-        tc_fence_after();
-        const uint32_t kb = base + C::K_OFF + st * C::TILE;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::ATOM + (kk & 3) * 32;
-          mma_bf16(T_S + (j & 1) * 128, make_sdesc(base + C::Q_OFF + off, 16, 1024), make_sdesc(kb + off, 16, 1024),
-                   id_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(s_full0 + 8 * (j & 1));
-      };
-      auto issue_dp = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(v_full0 + 8 * st, (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t vb = base + C::V_OFF + st * C::TILE;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::ATOM + (kk & 3) * 32;
-          mma_bf16(T_DP, make_sdesc(base + C::DO_OFF + off, 16, 1024), make_sdesc(vb + off, 16, 1024), id_s,
-                   kk > 0 ? 1u : 0u);
-        }
-        mma_commit(dp_full);
-        mma_commit(v_empty0 + 8 * st);
-      };
-      mbar_wait(qd_full, 0);
-      issue_s(0);
-      issue_dp(0);
-      for (int j = 0; j < nkb; ++j) {
-        if (j + 1 < nkb) issue_s(j + 1);  // S buffer (j+1)&1 was consumed by block j-1
-        mbar_wait(ds_full, j & 1);
-        tc_fence_after();
-        if (j + 1 < nkb) issue_dp(j + 1);  // the row threads have read dP_j
-        const uint32_t kb = base + C::K_OFF + (j % C::KST) * C::TILE;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dQ += dS K : A = dS (TMEM; each 64-key half packed in its first 32 columns)
-          mma_bf16_ts(T_DQ, T_S + (j & 1) * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
-                      make_sdesc(kb + kk * 2048, C::ATOM, 1024), id_q, (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(k_empty0 + 8 * (j % C::KST));
-      }
-      mma_commit(dq_done);
-    }
-    __syncwarp();
-  } else if (warp >= 4) {
-    // 8 warps: warp (q, hh) owns TMEM lane quarter q (query rows) and key-column half hh
-    const int q = warp & 3;
-    const int hh = (warp - 4) >> 2;
-    const int r = q * 32 + lane;  // query row == TMEM lane
-    const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
-    const float sl2 = scale * kLog2e;
-    const float lse_r = lse[(long long)bh * T + q0 + r] * kLog2e;
-    const float del_r = delta[(long long)bh * T + q0 + r];
-    for (int j = 0; j < nkb; ++j) {
-      const uint32_t ts = T_S + lo + (j & 1) * 128 + hh * 64;
-      mbar_wait(s_full0 + 8 * (j & 1), (j >> 1) & 1);
-      tc_fence_after();
-      float p[64];
-      {
-        uint32_t v0[32], v1[32];
-        tmem_ld32(ts, v0);
-        tmem_ld32(ts + 32, v1);
-        tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          p[k] = fast_exp2(__uint_as_float(v0[k]) * sl2 - lse_r);
-          p[32 + k] = fast_exp2(__uint_as_float(v1[k]) * sl2 - lse_r);
-        }
-      }
-      if (j == nkb - 1) {  // diagonal block: keys after the query
-#pragma unroll
-        for (int k = 0; k < 64; ++k)
-          if (hh * 64 + k > r) p[k] = 0.f;
-      }
-      mbar_wait(dp_full, j & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld32(T_DP + lo + hh * 64 + c * 32, v);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float d0 = p[c * 32 + 2 * k] * (__uint_as_float(v[2 * k]) - del_r) * scale;
-          const float d1 = p[c * 32 + 2 * k + 1] * (__uint_as_float(v[2 * k + 1]) - del_r) * scale;
-          pk[k] = pack_bf16(d0, d1);
-        }
-        // dS of this half's 64 keys packed into the half's first 32 columns, over S values
-        // this warp has already read (the other half's columns are never touched)
-        tmem_st16(ts + c * 16, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(ds_full);
-    }
-    mbar_wait(dq_done, 0);
-    tc_fence_after();
-    bf16* dq = dqkv + ((long long)row_base + q0 + r) * 3 * H * D + (long long)h * D;
-#pragma unroll 1
-    for (int c = hh * (D / 64); c < (hh + 1) * (D / 64); ++c) {
-      uint32_t v[32];
-      tmem_ld32(T_DQ + lo + c * 32, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 32; k += 8)
-        *reinterpret_cast<uint4*>(dq + c * 32 + k) =
-            make_uint4(pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
-                       pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
-                       pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
-                       pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 512);
-}
-
-template <int D>
-int attn_bwd_split_tc_launch(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
-                             int B, int T, int H, cudaStream_t s) {
-  CUtensorMap mq, mdo;
+namespace {
+int qkv_map(CUtensorMap* m, const void* p, int H, int D, int cols_mult, int rows_total, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols_mult * H * D, (cuuint64_t)rows_total};
+  cuuint64_t strides[1] = {(cuuint64_t)cols_mult * H * D * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  cuuint32_t box[2] = {64, 128};
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)3 * H * D, (cuuint64_t)B * T};
-    cuuint64_t strides[1] = {(cuuint64_t)3 * H * D * 2};
-    int rc = encode_tensor_map(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box,
-                               estr, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc) return rc;
-  }
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)H * D, (cuuint64_t)B * T};
-    cuuint64_t strides[1] = {(cuuint64_t)H * D * 2};
-    int rc = encode_tensor_map(&mdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(dout), dims, strides, box,
-                               estr, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc) return rc;
-  }
+  return encode_tensor_map(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <int D>
+cudaError_t bwd_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       BwdDqCfg<D>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             BwdDkdvCfg<D>::SMEM);
+  return e;
+}
+}  // namespace
+
+template <int D>
+int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const void* dout, void* dqkv, float* ws,
+                       int B, int T, int H, cudaStream_t s) {
+  if (T % 128) return set_error(ZPP_ERR_ARG, "attn_bwd: seq must be a multiple of 128");
+  const int BT = B * T;
+  CUtensorMap m_q128, m_kv64, m_kv128, m_q64, m_do128, m_do64;
+  int rc = qkv_map(&m_q128, qkv, H, D, 3, BT, 128);
+  if (!rc) rc = qkv_map(&m_kv64, qkv, H, D, 3, BT, 64);
+  if (!rc) rc = qkv_map(&m_kv128, qkv, H, D, 3, BT, 128);
+  if (!rc) rc = qkv_map(&m_q64, qkv, H, D, 3, BT, 64);
+  if (!rc) rc = qkv_map(&m_do128, dout, H, D, 1, BT, 128);
+  if (!rc) rc = qkv_map(&m_do64, dout, H, D, 1, BT, 64);
+  if (rc) return rc;
   static bool set = false;
   if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         DkdvCfg<D>::SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<D>::SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_split attr");
+    cudaError_t e = bwd_attrs<D>();
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd attr");
     set = true;
   }
+  const int BH = B * H;
+  float* delta = ws;
+  float* lse2 = ws + (long long)BH * T;
   const float scale = 1.f / sqrtf((float)D);
-  attn_bwd_dkdv_tc_kernel<D><<<dim3(T / 128, B * H), 384, DkdvCfg<D>::SMEM, s>>>(mq, mdo, lse, delta, (bf16*)dqkv, T,
-                                                                                   H, scale);
-  int rc = check_launch("attn_bwd_dkdv_tc");
+  const dim3 grid((T / 128) * BH);
+  attn_bwd_dq_kernel<D><<<grid, 384, BwdDqCfg<D>::SMEM, s>>>(m_q128, m_kv64, m_do128, (const bf16*)out, lse, delta, lse2,
+                                                               (bf16*)dqkv, T, H, BH, scale);
+  rc = check_launch("attn_bwd_dq");
   if (rc) return rc;
-  attn_bwd_dq_tc_kernel<D><<<dim3(T / 128, B * H), 384, DqCfg<D>::SMEM, s>>>(mq, mdo, lse, delta, (bf16*)dqkv, T, H,
-                                                                             scale);
-  return check_launch("attn_bwd_dq_tc");
+  attn_bwd_dkdv_kernel<D><<<grid, 384, BwdDkdvCfg<D>::SMEM, s>>>(m_kv128, m_q64, m_do64, lse2, delta, (bf16*)dqkv,
+                                                                   T, H, BH, scale);
+  return check_launch("attn_bwd_dkdv");
 }
 
-template int attn_bwd_split_tc_launch<64>(const void*, const void*, const float*, const float*, void*, int, int, int,
-                                          cudaStream_t);
-template int attn_bwd_split_tc_launch<128>(const void*, const void*, const float*, const float*, void*, int, int, int,
-                                           cudaStream_t);
+template int attn_bwd_tc_launch<64>(const void*, const void*, const float*, const void*, void*, float*, int, int,
+                                    int, cudaStream_t);
+template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, const void*, void*, float*, int, int,
+                                     int, cudaStream_t);
 
 int attention_bwd_tc_preload() {
-  cudaError_t e = cudaSuccess;
-  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             DkdvCfg<64>::SMEM));
-  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             DkdvCfg<128>::SMEM));
-  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             DqCfg<64>::SMEM));
-  e = (cudaError_t)(e | cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             DqCfg<128>::SMEM));
+  cudaError_t e = bwd_attrs<64>();
+  if (e == cudaSuccess) e = bwd_attrs<128>();
   return e == cudaSuccess ? ZPP_OK : set_cuda_error(e, "attention_bwd_tc preload");
 }
 
 }  // namespace zpp
+
+#ifdef ZPP_TRACE
+extern "C" int zpp_debug_attn_trace(void* host_out) {
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, zpp::g_attn_trace, sizeof(zpp::g_attn_trace));
+  return e == cudaSuccess ? 0 : zpp::set_cuda_error(e, "trace");
+}
+#endif

@@ -34,7 +34,6 @@ namespace zpp {
 
 typedef __nv_bfloat16 bf16;
 
-constexpr int kFwd2DefaultEmu = 0;  // measured: the FMA-pipe exp2 costs more energy than it saves (power-capped)
 
 template <int D>
 struct Fwd2Cfg {
@@ -48,9 +47,7 @@ struct Fwd2Cfg {
   static_assert(SMEM <= 232448, "smem budget");
 };
 
-// EMU: of every 8 packed column pairs, how many compute exp2 on the FMA pipe (exp2_poly)
-// instead of the MUFU unit -- two softmax warpgroups per SM would otherwise be MUFU-bound.
-template <int D, int EMU>
+template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, bf16* __restrict__ out, float* __restrict__ lse,
                         int T, int H, int BH, float scale_log2) {
@@ -251,9 +248,8 @@ __global__ void __launch_bounds__(384, 1)
         for (int k = 0; k < 16; ++k) {
           const float a0 = fmaf(x[c4 * 32 + 2 * k], scale_log2, -m_use);
           const float a1 = fmaf(x[c4 * 32 + 2 * k + 1], scale_log2, -m_use);
-          const bool emu = (k & 7) >= 8 - EMU;
-          const float e0 = emu ? exp2_poly(a0) : fast_exp2(a0);
-          const float e1 = emu ? exp2_poly(a1) : fast_exp2(a1);
+          const float e0 = fast_exp2(a0);
+          const float e1 = fast_exp2(a1);
           ps[(2 * k) & 7] += e0;
           ps[(2 * k + 1) & 7] += e1;
           pk[k] = pack_bf16(e0, e1);
@@ -291,10 +287,9 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-template <int D, int EMU>
+template <int D>
 static cudaError_t fwd2_attr() {
-  return cudaFuncSetAttribute(attn_fwd2_tc_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Fwd2Cfg<D>::SMEM);
+  return cudaFuncSetAttribute(attn_fwd2_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
 }
 
 template <int D>
@@ -309,25 +304,15 @@ int attn_fwd2_tc_launch(const void* qkv, void* out, float* lse, int B, int T, in
   int rc = encode_tensor_map(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box, estr,
                              CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  static int emu = -1;
-  if (emu < 0) {
-    const char* ev = getenv("ZPP_ATTN_EMU");
-    emu = ev ? atoi(ev) : kFwd2DefaultEmu;
-    cudaError_t e = emu >= 3 ? fwd2_attr<D, 3>() : emu == 2 ? fwd2_attr<D, 2>() : fwd2_attr<D, 0>();
-    if (e != cudaSuccess) {
-      emu = -1;
-      return set_cuda_error(e, "attn_fwd2_tc attr");
-    }
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = fwd2_attr<D>();
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_fwd2_tc attr");
+    set = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   const int BH = B * H;
-  const dim3 grid((T / 256) * BH);
-  if (emu >= 3)
-    attn_fwd2_tc_kernel<D, 3><<<grid, 384, C::SMEM, s>>>(m, (bf16*)out, lse, T, H, BH, scale_log2);
-  else if (emu == 2)
-    attn_fwd2_tc_kernel<D, 2><<<grid, 384, C::SMEM, s>>>(m, (bf16*)out, lse, T, H, BH, scale_log2);
-  else
-    attn_fwd2_tc_kernel<D, 0><<<grid, 384, C::SMEM, s>>>(m, (bf16*)out, lse, T, H, BH, scale_log2);
+  attn_fwd2_tc_kernel<D><<<dim3((T / 256) * BH), 384, C::SMEM, s>>>(m, (bf16*)out, lse, T, H, BH, scale_log2);
   return check_launch("attn_fwd2_tc");
 }
 
@@ -335,12 +320,8 @@ template int attn_fwd2_tc_launch<64>(const void*, void*, float*, int, int, int, 
 template int attn_fwd2_tc_launch<128>(const void*, void*, float*, int, int, int, cudaStream_t);
 
 int attention_fwd2_preload() {
-  cudaError_t e = fwd2_attr<64, 0>();
-  if (e == cudaSuccess) e = fwd2_attr<64, 2>();
-  if (e == cudaSuccess) e = fwd2_attr<64, 3>();
-  if (e == cudaSuccess) e = fwd2_attr<128, 0>();
-  if (e == cudaSuccess) e = fwd2_attr<128, 2>();
-  if (e == cudaSuccess) e = fwd2_attr<128, 3>();
+  cudaError_t e = fwd2_attr<64>();
+  if (e == cudaSuccess) e = fwd2_attr<128>();
   return e == cudaSuccess ? ZPP_OK : set_cuda_error(e, "attention_fwd2 preload");
 }
 

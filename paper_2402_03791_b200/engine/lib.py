@@ -26,7 +26,6 @@ _SIGS = {
                          P, P, c_size, P, c_size, c_stream]),
     "zpp_gemm_set_cta_group": (c_int, [c_int]),
     "zpp_gemm_set_streamk": (c_int, [c_int]),
-    "zpp_attn_set_impl": (c_int, [c_int]),
     "zpp_attn_fwd": (c_int, [P, P, P, c_int, c_int, c_int, c_int, c_stream]),
     "zpp_attn_bwd": (c_int, [P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_stream]),
     "zpp_attn_bwd_workspace_floats": (c_longlong, [c_int, c_int, c_int, c_int]),
@@ -85,8 +84,6 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     _lib = lib
-    if os.environ.get("ZPP_ATTN_IMPL"):  # A/B switch for the attention kernels (see ops.set_attn_impl)
-        check(lib.zpp_attn_set_impl(int(os.environ["ZPP_ATTN_IMPL"])), "zpp_attn_set_impl")
     return lib
 
 

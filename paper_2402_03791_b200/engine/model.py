@@ -68,8 +68,10 @@ class GPTSpec:
             raise ValueError("hidden must be divisible by heads")
         if self.head_dim not in (64, 128):
             raise ValueError("head_dim must be 64 or 128 (attention kernels)")
-        if self.seq_len % 64 or self.hidden % 64 or self.vocab % 64:
-            raise ValueError("seq_len, hidden and vocab must be multiples of 64")
+        if self.seq_len % 128:
+            raise ValueError("seq_len must be a multiple of 128 (attention tiles)")
+        if self.hidden % 64 or self.vocab % 64:
+            raise ValueError("hidden and vocab must be multiples of 64")
 
     @property
     def head_dim(self) -> int:

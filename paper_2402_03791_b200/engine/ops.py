@@ -186,12 +186,6 @@ def gelu(u, g, stream=None):
     lib.call("zpp_gelu_fwd", _p(u), _p(g), u.numel(), _s(stream))
 
 
-def set_attn_impl(impl: int) -> None:
-    """0 auto (tcgen05 kernels when seq % 128 == 0; forward with two query tiles per CTA when
-    seq % 256 == 0), 1 mma.sync FlashAttention-2 tiles, 2 tcgen05 one query tile per CTA."""
-    lib.call("zpp_attn_set_impl", impl)
-
-
 def attn_fwd(qkv, out, lse, batch, seq, heads, head_dim, stream=None):
     _count(1)
     lib.call("zpp_attn_fwd", _p(qkv), _p(out), _p(lse), batch, seq, heads, head_dim, _s(stream))
@@ -202,7 +196,9 @@ def attn_bwd_workspace(batch, seq, heads, head_dim) -> int:
 
 
 def attn_bwd(qkv, out, lse, dout, dqkv, workspace, batch, seq, heads, head_dim, stream=None):
-    _count(3)
+    """dQ kernel (also writes delta = rowsum(O dO) and lse*log2e into ``workspace``), then the
+    dK/dV kernel; deterministic (no atomics)."""
+    _count(2)
     lib.call("zpp_attn_bwd", _p(qkv), _p(out), _p(lse), _p(dout), _p(dqkv), _p(workspace), batch, seq,
              heads, head_dim, _s(stream))
 

@@ -43,8 +43,8 @@ def test_pure_host_entry_points(so):
     rc = so.zpp_gemm(None, 0, 7, None, 0, 8, None, 8, 0, 8, 8, 0, None, None, 0, None, 0, 0)
     assert rc == 1001 and b"empty" in so.zpp_last_error()
     rc = so.zpp_attn_fwd(None, None, None, 1, 100, 2, 64, 0)
-    assert rc == 1001 and b"multiple of 64" in so.zpp_last_error()
-    assert so.zpp_attn_bwd_workspace_floats(1, 128, 2, 64) == 2 * 128 + 128 * 2 * 64
+    assert rc == 1001 and b"multiple of 128" in so.zpp_last_error()
+    assert so.zpp_attn_bwd_workspace_floats(1, 128, 2, 64) == 2 * 2 * 128
 
 
 def test_nccl_loads_from_torch_wheel(so):

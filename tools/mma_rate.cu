@@ -5,7 +5,7 @@
 #include "ptx.cuh"
 using namespace zpp;
 
-template <int CG, int N, int COMMIT, bool AMN = false, bool BMN = false>
+template <int CG, int N, int COMMIT, bool AMN = false, bool BMN = false, bool TS = false>
 __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, bar2;
@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
   const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); mbar_init(smem_u32(&bar2), 1 << 20); fence_mbar_init(); }
-  if (warp == 0) { if (CG == 2) tmem_alloc2(smem_u32(&tslot), 256); else tmem_alloc(smem_u32(&tslot), 256); }
+  if (warp == 0) { if (CG == 2) tmem_alloc2(smem_u32(&tslot), 512); else tmem_alloc(smem_u32(&tslot), 512); }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
       for (int k = 0; k < 4; ++k) {
         const uint64_t ka = AMN ? (uint64_t)(128 * k) : (uint64_t)(2 * k), kb = BMN ? (uint64_t)(128 * k) : (uint64_t)(2 * k);
         if (CG == 2) mma_bf16_2sm(tmem, ad + ka, bd + kb, idesc, 1u);
+        else if (TS) mma_bf16_ts(tmem, tmem + 256 + 8 * k, bd + kb, idesc, 1u);
         else mma_bf16(tmem, ad + ka, bd + kb, idesc, 1u);
       }
       if (COMMIT == 1) { if (CG == 2) mma_commit_2sm(smem_u32(&bar2), 0x3); else mma_commit(smem_u32(&bar2)); }
@@ -41,14 +42,64 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
   if (CG == 2 && !leader && threadIdx.x == 0) mbar_wait(smem_u32(&bar), 0);
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
-  if (warp == 0) { if (CG == 2) tmem_dealloc2(tmem, 256); else tmem_dealloc(tmem, 256); }
+  if (warp == 0) { if (CG == 2) tmem_dealloc2(tmem, 512); else tmem_dealloc(tmem, 512); }
 }
 
-template <int CG, int N, int COMMIT, bool AMN = false, bool BMN = false>
+// whole-warp issue with elect.sync (uniform descriptors), 8 K-steps per iteration
+template <int N, bool TS>
+__global__ void __launch_bounds__(128, 1) mma_loop_w(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc(smem_u32(&tslot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp == 0) {
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, false, false);
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t bd = make_sdesc(base + 16384 + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
+        if (TS) mma_bf16_ts_w(tmem, tmem + 256 + 8 * (k & 3), bd, idesc, 1u);
+        else mma_bf16_w(tmem, make_sdesc(base + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024), bd, idesc, 1u);
+      }
+    }
+    mma_commit_w(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    unsigned long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N, bool TS>
+void run_w(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  auto k = mma_loop_w<N, TS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  const int iters = 1024;
+  k<<<148, 128, 64 * 1024>>>(16, d);
+  k<<<148, 128, 64 * 1024>>>(iters, d);
+  cudaError_t err = cudaDeviceSynchronize();
+  unsigned long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  printf("%-22s %s  %.1f cycles/MMA-instr (floor %d)\n", name, cudaGetErrorString(err), double(cyc) / (iters * 8),
+         128 * N / 256);
+}
+
+template <int CG, int N, int COMMIT, bool AMN = false, bool BMN = false, bool TS = false>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 8);
-  auto k = mma_loop<CG, N, COMMIT, AMN, BMN>;
+  auto k = mma_loop<CG, N, COMMIT, AMN, BMN, TS>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = 64 * 1024;
@@ -74,5 +125,17 @@ int main() {
   run<2, 256, 1, false, true>("cta2 K/MN");
   run<2, 256, 1, true, true>("cta2 MN/MN");
   run<1, 256, 1, true, true>("cta1 MN/MN");
+  run<1, 256, 0>("cta1 N256 SS K/K");
+  run<1, 128, 0>("cta1 N128 SS K/K");
+  run<1, 64, 0>("cta1 N64 SS K/K");
+  run<1, 32, 0>("cta1 N32 SS K/K");
+  run<1, 128, 0, false, true>("cta1 N128 SS K/MN");
+  run<1, 128, 0, false, true, true>("cta1 N128 TS K/MN");
+  run<1, 64, 0, false, false, true>("cta1 N64 TS K/K");
+  run<1, 256, 0, false, true, true>("cta1 N256 TS K/MN");
+  run_w<64, false>("warp N64 SS");
+  run_w<64, true>("warp N64 TS");
+  run_w<32, false>("warp N32 SS");
+  run_w<128, false>("warp N128 SS");
   return 0;
 }
