@@ -59,9 +59,10 @@ int zpp_gemm(const void* A, int a_mn_major, long long lda, const void* B, int b_
 /* CTA-group policy for zpp_gemm: 0 = auto (CTA pairs, cta_group::2, when M > 256),
  * 1 = single-CTA tiles only, 2 = prefer pairs.  Process-wide. */
 int zpp_gemm_set_cta_group(int cg);
-/* Hybrid data-parallel + stream-K split of the last partial wave (default on; the
- * ZPP_GEMM_STREAMK env var sets the initial value).  Needs the per-stream workspaces
- * that zpp_preload_kernels allocates; without them GEMMs run unsplit.  Process-wide. */
+/* Hybrid data-parallel + stream-K split of the last partial wave (default on).  Process-wide.
+ * zpp_gemm needs zpp_preload_kernels() first: it allocates the per-stream tile-scheduler
+ * counters (up to 32 launching streams) and stream-K workspaces; the launch path itself never
+ * allocates or synchronises, so GEMMs can be captured in CUDA graphs. */
 int zpp_gemm_set_streamk(int on);
 
 /* ---- causal multi-head attention, qkv packed [b, s, 3, heads, d] bf16 --------- */

@@ -64,7 +64,7 @@ struct SkParams {
   int pieces;
   float* ws;        // [(sk_tile * pieces + piece)][BN/32][TILE_M/32][8][32 lanes] float4 partials
   unsigned* flags;  // [sk_tile][CG][4 epilogue warps] arrival counters, re-armed by the finisher
-  unsigned long long* trace;  // ZPP_GEMM_TRACE: [cta][GEMM_TRACE_ITEMS][6] globaltimer stamps, or null
+  unsigned long long* trace;  // debug build (ZPP_TRACE): [cta][GEMM_TRACE_ITEMS][6] globaltimer stamps, or null
 };
 constexpr int GEMM_TRACE_ITEMS = 32;
 
@@ -581,19 +581,29 @@ static int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const v
                            CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// Scheduler counters: [tile counter, CTAs done] per launch slot, zeroed once and re-armed
-// by the last CTA of each launch; slots rotate so concurrent launches on other streams
-// do not share one.
-static unsigned* sched_slot() {
-  constexpr int NSLOT = 256;
-  static unsigned* buf = nullptr;
-  static unsigned next = 0;
-  if (!buf) {
-    if (cudaMalloc(&buf, NSLOT * 2 * sizeof(unsigned)) != cudaSuccess) return nullptr;
-    cudaMemset(buf, 0, NSLOT * 2 * sizeof(unsigned));
-    cudaDeviceSynchronize();
-  }
-  return buf + 2 * (next++ % NSLOT);
+// Scheduler counters: [tile counter, CTAs done] per stream, zeroed at preload and re-armed by
+// the last CTA of each launch.  Launches on one stream are ordered, so a stream owns one
+// slot; concurrent GEMMs on different streams never share a counter.  Allocated in
+// gemm_preload() -- the launch path never allocates or synchronises.
+constexpr int SCHED_STREAMS = 32;
+struct SchedSlot {
+  cudaStream_t stream;
+  bool used;
+};
+static SchedSlot g_sched_tab[SCHED_STREAMS];
+static unsigned* g_sched = nullptr;
+
+static unsigned* sched_slot(cudaStream_t s) {
+  if (!g_sched) return nullptr;
+  for (int i = 0; i < SCHED_STREAMS; ++i)
+    if (g_sched_tab[i].used && g_sched_tab[i].stream == s) return g_sched + 2 * i;
+  for (int i = 0; i < SCHED_STREAMS; ++i)
+    if (!g_sched_tab[i].used) {
+      g_sched_tab[i].used = true;
+      g_sched_tab[i].stream = s;
+      return g_sched + 2 * i;
+    }
+  return nullptr;
 }
 
 // Stream-K workspaces: one per stream that launches split GEMMs (launches on one stream
@@ -611,12 +621,15 @@ struct SkCtx {
   unsigned* flags;
 };
 static SkCtx g_sk[SK_CTX];
-static unsigned long long* g_gemm_trace = nullptr;  // ZPP_GEMM_TRACE=1: last launch's timeline
+static unsigned long long* g_gemm_trace = nullptr;  // debug build (ZPP_TRACE): last launch's timeline
 static bool g_sk_ready = false;
-static int g_sk_mode = -1;  // ZPP_GEMM_STREAMK: 0 off, 1 on (default)
+static int g_sk_mode = 1;  // stream-K split of the last partial wave (zpp_gemm_set_streamk)
 
 static int sk_alloc() {
   if (g_sk_ready) return ZPP_OK;
+  if (cudaMalloc(&g_sched, SCHED_STREAMS * 2 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(g_sched, 0, SCHED_STREAMS * 2 * sizeof(unsigned)) != cudaSuccess)
+    return set_error(ZPP_ERR_CUDA, "gemm: scheduler counter allocation failed");
   for (auto& c : g_sk) {
     if (cudaMalloc(&c.ws, SK_WS_FLOATS * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&c.flags, SK_FLAGS * sizeof(unsigned)) != cudaSuccess)
@@ -625,12 +638,13 @@ static int sk_alloc() {
       return set_error(ZPP_ERR_CUDA, "gemm: stream-K flag init failed");
     c.used = false;
   }
-  const char* tr = getenv("ZPP_GEMM_TRACE");
-  if (tr && atoi(tr) && !g_gemm_trace) {
+#ifdef ZPP_TRACE
+  {
     const size_t bytes = 148ull * GEMM_TRACE_ITEMS * 6 * sizeof(unsigned long long);
     if (cudaMalloc(&g_gemm_trace, bytes) != cudaSuccess) return set_error(ZPP_ERR_CUDA, "gemm trace alloc");
     cudaMemset(g_gemm_trace, 0, bytes);
   }
+#endif
   cudaDeviceSynchronize();
   g_sk_ready = true;
   return ZPP_OK;
@@ -654,26 +668,8 @@ static SkCtx* sk_ctx(cudaStream_t s) {
 // round trip and pipeline refill).
 static SkParams sk_plan(int tiles, int units, int num_k, int tile_m, int bn, cudaStream_t s) {
   SkParams sk{tiles, 1, nullptr, nullptr, g_gemm_trace};
-  if (g_sk_mode < 0) {
-    const char* e = getenv("ZPP_GEMM_STREAMK");
-    g_sk_mode = e ? atoi(e) : 1;
-  }
   if (!g_sk_mode || tiles <= units || tiles % units == 0) return sk;
   const int full = tiles / units, r = tiles % units;
-  static int force = -1;  // ZPP_GEMM_SK_FORCE=p: tuning override of the piece count
-  if (force < 0) {
-    const char* e = getenv("ZPP_GEMM_SK_FORCE");
-    force = e ? atoi(e) : 0;
-  }
-  if (force > 0 && force <= SK_MAX_PIECES) {
-    SkCtx* c = sk_ctx(s);
-    if (!c) return sk;
-    sk.dp_tiles = full * units;
-    sk.pieces = force;
-    sk.ws = c->ws;
-    sk.flags = c->flags;
-    return sk;
-  }
   // Measured (tools/gemm_trace.py): parking a 128 KB partial ~6 us and summing it back
   // ~7 us per piece -- the read-back is latency-bound at ~32 KB in flight per SM -- so one
   // extra piece costs ~22 k-blocks (0.34 us each at 256x256 pair tiles).
@@ -724,12 +720,7 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
     attr_set = true;
   }
   const int tiles = ((M + GEMM_BM * CG - 1) / (GEMM_BM * CG)) * ((N + BN - 1) / BN);
-  static int reserve = -1;
-  if (reserve < 0) {
-    const char* e = getenv("ZPP_GEMM_RESERVE_SMS");
-    reserve = e ? atoi(e) : 0;
-  }
-  const int units = (num_sms() - reserve) / CG;
+  const int units = num_sms() / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -743,8 +734,10 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  unsigned* sched = sched_slot();
-  if (!sched) return set_error(ZPP_ERR_CUDA, "gemm: scheduler buffer allocation failed");
+  unsigned* sched = sched_slot(stream);
+  if (!sched)
+    return set_error(ZPP_ERR_ARG, g_sched ? "gemm: more than 32 launching streams"
+                                          : "gemm: call zpp_preload_kernels() before the first GEMM");
   const SkParams sk = sk_plan(tiles, grid / CG, (K + GEMM_BK - 1) / GEMM_BK, GEMM_BM * CG, BN, stream);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, M, N, K, ep, sk, sched);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
@@ -792,6 +785,7 @@ static int g_cg_pref = 0;  // 0 = auto, 1 = force single-CTA tiles, 2 = prefer p
 
 // Debug: copy the last traced launch's timeline ([cta][32 items][item, mma0, mma1, epi0,
 // epi_acc, epi1] globaltimer ns) to host memory; returns the number of u64 copied.
+#ifdef ZPP_TRACE  // debug build only (make trace)
 extern "C" long long zpp_gemm_trace_dump(unsigned long long* host, long long max_u64) {
   if (!zpp::g_gemm_trace) return 0;
   long long n = 148LL * zpp::GEMM_TRACE_ITEMS * 6;
@@ -801,6 +795,7 @@ extern "C" long long zpp_gemm_trace_dump(unsigned long long* host, long long max
   cudaMemset(zpp::g_gemm_trace, 0, 148ull * zpp::GEMM_TRACE_ITEMS * 6 * 8);
   return n;
 }
+#endif
 
 extern "C" int zpp_gemm_set_streamk(int on) {
   zpp::g_sk_mode = on ? 1 : 0;

@@ -344,12 +344,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
 }
 
 static int colred_splits(int rows, int strips) {
-  static int waves = -1;  // target blocks = waves x SMs (ZPP_CR_WAVES, A/B experiments only)
-  if (waves < 0) {
-    const char* e = getenv("ZPP_CR_WAVES");
-    waves = e ? atoi(e) : 2;
-    if (waves < 1) waves = 2;
-  }
+  constexpr int waves = 2;  // target blocks = 2 x SMs (4 and 8 measured slower, profiles/r01d_colred_ab.txt)
   int s = 1;
   while (s < CR_MAX_SPLIT && strips * s < waves * num_sms() && rows / (2 * s) >= 64) s *= 2;
   return s;

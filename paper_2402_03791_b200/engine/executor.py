@@ -39,7 +39,6 @@ from . import lib, ops
 from .model import GPTSpec, StageLayout, init_offset, optimizer_sub, shard_init_ranges, stage_layout
 
 BF16, F32 = torch.bfloat16, torch.float32
-_TRACE = os.environ.get("ZPP_TRACE") == "1"
 
 
 def rank_coords(rank: int, n: int, P: int, D: int) -> tuple[int, int, int]:
@@ -181,7 +180,12 @@ class Runtime:
 
     def __init__(self, spec: GPTSpec, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
-                 timeline: bool = False):
+                 timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
+                 aux_stream: bool = True, host_trace: bool = False):
+        """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
+        task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
+        reductions on a side stream; ``host_trace``: print each task as it is enqueued
+        (first two steps, debugging)."""
         if world != cfg.pp_size * cfg.dp_size * cfg.inter_node_dp:
             raise ValueError(f"world size {world} != n*P*D = "
                              f"{cfg.inter_node_dp * cfg.pp_size * cfg.dp_size}")
@@ -217,24 +221,23 @@ class Runtime:
         self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
         self.s_act_send, self.s_act_recv, self.s_grad_send, self.s_grad_recv = mk(), mk(), mk(), mk()
         # parameter-gradient column reductions (bias, norm gamma / beta) only feed RS / OPT:
-        # they run on this side stream beside the next GEMMs (ZPP_AUX_STREAM=0 keeps them inline)
-        self.s_aux = mk() if os.environ.get("ZPP_AUX_STREAM", "1") != "0" else self.s_comp
+        # they run on this side stream beside the next GEMMs (aux_stream=False keeps them inline)
+        self.s_aux = mk() if aux_stream else self.s_comp
         # Early optimizer: a stage's AdamW starts on its own stream as soon as the stage's
         # gradients are final (its last W at D == 1, layer by layer; its last RS_GRAD at
         # D > 1), overlapping the remaining B / W work instead of trailing the step.  The OPT
-        # task still orders everything after it (ZPP_EARLY_OPT=0: OPT runs it all, as before).
+        # task still orders everything after it (early_opt=False: OPT runs it all).
         # Default on at D > 1, where it lets the next step's AG_PARAM of a stage start early;
         # at D == 1 there is nothing to overlap but the GEMMs, which under the power cap only
         # slows them (measured: profiles/r01c_ab_n1_aux_earlyopt_b2.txt), so it is off there.
-        mode = os.environ.get("ZPP_EARLY_OPT", "auto")
-        self.early_opt = self.n == 1 and (mode == "1" or (mode == "auto" and self.D > 1))
+        self.early_opt = self.n == 1 and (self.D > 1 if early_opt is None else bool(early_opt))
         self.s_opt = mk()
-        # CUDA-graph mode (ZPP_CUDA_GRAPH=1; one rank, no early optimizer): the task list up to
+        # CUDA-graph mode (cuda_graph=True; one rank, no early optimizer): the task list up to
         # OPT is captured once, on the second step, and replayed; OPT runs eagerly after it
         # (AdamW's bias correction depends on the step number).  Shapes, buffers and the task
         # order are static, so a replay is the same launches without the host in the loop.
-        self.graph_mode = (os.environ.get("ZPP_CUDA_GRAPH", "0") == "1" and world == 1
-                           and cfg.inter_node_dp == 1)
+        self.graph_mode = bool(cuda_graph) and world == 1 and cfg.inter_node_dp == 1
+        self.host_trace = host_trace
         self._graph = None
         self._final_w, self._final_rs = {}, {}
         for i, t in enumerate(self.tasks):
@@ -354,7 +357,7 @@ class Runtime:
         comp = self.s_comp
         comp.wait_stream(torch.cuda.current_stream(self.dev))
         t_start = self._record(comp, True)
-        trace = _TRACE and self.step_count <= 2
+        trace = self.host_trace and self.step_count <= 2
         with torch.cuda.stream(comp):
             ops.zero(self.loss_sum, stream=comp)
             self._opt_done: set = set()

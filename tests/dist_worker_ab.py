@@ -1,6 +1,6 @@
 """One rank of an A/B determinism check under torchrun (or alone at world 1): the same
 ZeroPP steps run twice in fresh runtimes, with the early optimizer on and off
-(ZPP_EARLY_OPT); fp32 master shards and bf16 shards must be bit-identical -- the early
+(Runtime(early_opt=...)); fp32 master shards and bf16 shards must be bit-identical -- the early
 (chunked, overlapped) AdamW and the per-stage AG gating only reorder work, and every
 gradient path is deterministic (no fp32 atomics).  The reported loss is an fp32 atomic
 sum over token rows, so it is compared to 1e-6 relative.
@@ -25,9 +25,8 @@ from paper_2402_03791_b200.engine import GPTSpec  # noqa: E402
 
 
 def run(early: str, P, D, B, U, V, steps, rank, world):
-    os.environ["ZPP_EARLY_OPT"] = early
     rt, _, _, res = run_engine_step(GPTSpec.tiny(), P, D, B, U, V, rank=rank, world=world, steps=steps,
-                                    timeline=False)
+                                    timeline=False, rt_kw={"early_opt": early == "1"})
     assert rt.early_opt == (early == "1")
     losses = [r.loss_sum.item() for r in res]
     state = {s: (st.master.cpu(), st.shard_bf16.cpu()) for s, st in rt.stages.items()}

@@ -94,9 +94,9 @@ def rank_tokens(tokens_step: torch.Tensor, z: int):
 
 
 def run_engine_step(spec, P, D, B, U, V, rank=0, world=1, steps=1, timeline=True, snapshot_init=False,
-                    **cfg_kw):
+                    rt_kw=None, **cfg_kw):
     model, cfg, pl, sched = build(spec, P, D, B, U, V, **cfg_kw)
-    rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=timeline)
+    rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=timeline, **(rt_kw or {}))
     if snapshot_init:  # fp32 masters before step 1 (whole stages when P x D = 1 x 1)
         torch.cuda.synchronize()
         rt.init_master = {s: st.master.clone() for s, st in rt.stages.items()}

@@ -162,15 +162,14 @@ def test_early_optimizer_is_bit_identical(tmp_path, P, D, B, U, V):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
-def test_cuda_graph_step_is_bit_identical(monkeypatch):
-    """ZPP_CUDA_GRAPH=1: steps 2.. replay a captured graph of the task list up to OPT; 4 steps
+def test_cuda_graph_step_is_bit_identical():
+    """Runtime(cuda_graph=True): steps 2.. replay a captured graph of the task list up to OPT; 4 steps
     give the same fp32 masters / bf16 params bit for bit as 4 eager steps."""
     spec = GPTSpec.tiny()
     out = {}
     for mode in ("0", "1"):
-        monkeypatch.setenv("ZPP_CUDA_GRAPH", mode)
-        monkeypatch.setenv("ZPP_EARLY_OPT", "0")
-        rt, _, _, res = run_engine_step(spec, 1, 1, 4, 2, 2, steps=4, timeline=False)
+        rt, _, _, res = run_engine_step(spec, 1, 1, 4, 2, 2, steps=4, timeline=False,
+                                        rt_kw={"cuda_graph": mode == "1", "early_opt": False})
         assert rt.graph_mode == (mode == "1") and (rt._graph is not None) == (mode == "1")
         out[mode] = ([r.loss_sum.item() for r in res],
                      {s: (st.master.cpu(), st.shard_bf16.cpu()) for s, st in rt.stages.items()})

@@ -1,4 +1,4 @@
-"""Timeline of one GEMM launch (ZPP_GEMM_TRACE=1).  usage: gemm_trace.py M N K a_t b_t [bf16|f32|f32acc]"""
+"""Timeline of one GEMM launch (debug build: make -C paper_2402_03791_b200/csrc trace).  usage: gemm_trace.py M N K a_t b_t [bf16|f32|f32acc]"""
 import ctypes
 import os
 import sys
@@ -6,9 +6,12 @@ import sys
 import numpy as np
 import torch
 
-os.environ["ZPP_GEMM_TRACE"] = "1"
+
 sys.path.insert(0, '.')
-from paper_2402_03791_b200.engine import lib, ops  # noqa: E402
+from paper_2402_03791_b200.engine import lib  # noqa: E402
+
+lib.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libzpp_trace.so")
+from paper_2402_03791_b200.engine import ops  # noqa: E402
 
 M, N, K = (int(x) for x in sys.argv[1:4])
 at, bt = sys.argv[4] == '1', sys.argv[5] == '1'
