@@ -14,9 +14,12 @@ e2e    : same metric through the public API ``execute(...)`` with per-step H2D c
          step's token ids/labels from pinned host memory and a D2H read of the loss
 roofline: dominant kernel = the tcgen05 GEMM; achieved = algorithmic GEMM FLOPs of the timed
          steps / summed CUDA-event durations of those GEMM launches (on their stream)
-cpu_baseline / --impl reference: the CPU fp32 oracle (oracle/gpt_oracle.py) timed on this
-         host on a bounded sample (1 GPT-6.2B layer + LM head, 2048 tokens, fwd+bwd),
-         extrapolated to the full model by model FLOPs.
+cpu_baseline: the CPU fp32 oracle (oracle/gpt_oracle.py) timed on this host on a bounded
+         sample (1 GPT-6.2B layer + LM head, 2048 tokens, fwd+bwd), extrapolated to the full
+         model by model FLOPs (labelled ``extrapolated``).
+--impl reference: that CPU figure, plus the reference package's own generate / validate /
+         simulate timed for this config (baseline/_ref) and a fully measured C1 oracle step
+         (see run_reference).
 """
 
 from __future__ import annotations
@@ -43,7 +46,8 @@ SPLITS = {1: (1, 1, 8, 2, 1, 2), 2: (2, 1, 16, 8, 2, 2), 4: (2, 2, 16, 8, 2, 2),
 # other BASELINE configs (parity cases; measured with --model / --split, not the headline line)
 MODELS = {"gpt-6.2b": ("gpt_6p2b", "GPT-6.2B (L32 h4096 a32 s2048 V50304, untied head)"),
           "gpt-1.3b": ("gpt_1p3b", "GPT-1.3B (L24 h2048 a16 s2048 V50304, untied head)"),
-          "llama-7b": ("llama_7b", "LLaMA-7B (L32 h4096 a32 s4096 V32000, SwiGLU 11008, RoPE, RMSNorm)")}
+          "llama-7b": ("llama_7b", "LLaMA-7B (L32 h4096 a32 s4096 V32000, SwiGLU 11008, RoPE, RMSNorm)"),
+          "gpt-13b": ("gpt_13b", "GPT-13B (L40 h5120 a40 s2048 V50304, untied head)")}
 PEAK_DENSE_TF = 2250.0
 
 
@@ -308,29 +312,122 @@ def _split(args):
     return P, D, B, U, V, b
 
 
+def reference_schedule_path(args) -> dict:
+    """The reference's OWN CPU path for this config, timed here: ``zeroppsim`` generate +
+    validate + simulate (`schedules.py:555-567`, `validation.py:99-135`, `simulation.py:90-158`),
+    imported read-only from ``baseline/_ref`` (pip-installed from the reference, git-ignored,
+    shipped to the GPU box).  Single-threaded pure Python, as the reference runs.  Also checks
+    that its schedule is the one this engine executes (same per-device task ids)."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "zeroppsim")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md, reference arm)"}
+    sys.path.insert(0, ref_dir)
+    import zeroppsim as R
+    from paper_2402_03791_b200 import ModelSpec, ParallelConfig, generate, make_placement
+    from paper_2402_03791_b200.engine import GPTSpec
+    P, D, B, U, V, mbs = _split(args)
+    spec = getattr(GPTSpec, MODELS[args.model][0])(microbatch_samples=mbs)
+    mk = dict(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
+    pk = dict(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V, microbatch_samples=mbs)
+    m, c = R.ModelSpec(**mk), R.ParallelConfig(**pk)
+    pl = R.make_placement(c, m)
+    costs = R.CommCostModel(intra_node_bandwidth=900e9, inter_node_bandwidth=50e9)
+    reps = 20
+    t = {"generate": [], "validate": [], "simulate": []}
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sched = R.generate(m, c, pl)
+        t1 = time.perf_counter()
+        bad = R.validate(sched, pl, c)
+        t2 = time.perf_counter()
+        sim = R.simulate(sched, m, c, pl, costs)
+        t3 = time.perf_counter()
+        t["generate"].append(t1 - t0)
+        t["validate"].append(t2 - t1)
+        t["simulate"].append(t3 - t2)
+    ours = generate(ModelSpec(**mk), ParallelConfig(**pk), make_placement(ParallelConfig(**pk), ModelSpec(**mk)))
+    same = [[x.task_id for x in d] for d in sched.per_device] == [[x.task_id for x in d] for d in ours.per_device]
+    out = {f"{k}_ms": round(statistics.median(v) * 1e3, 3) for k, v in t.items()}
+    out.update({"cores": 1, "tasks": sched.task_count(), "violations": len(bad), "makespan_units": sim.makespan,
+                "same_task_order_as_engine": same, "repeats": reps,
+                "source": "zeroppsim 0.1.0 from baseline/_ref (the reference package itself)"})
+    return out
+
+
+def c1_oracle_step(threads: int) -> dict:
+    """A MEASURED CPU step of BASELINE config C1 (tiny GPT L4 h256 s128, P2 x D2, B8 U4 V2):
+    the fp32 oracle's forward + backward + AdamW over the global batch (2 x 8 x 128 tokens),
+    the whole step, nothing extrapolated."""
+    import torch
+    from oracle.gpt_oracle import make_tokens, oracle_step
+    from oracle.init_oracle import init_values
+    from paper_2402_03791_b200 import ModelSpec, ParallelConfig, make_placement
+    from paper_2402_03791_b200.engine import GPTSpec
+    from paper_2402_03791_b200.engine.model import init_offset, stage_layout
+    torch.set_num_threads(threads)
+    spec = GPTSpec.tiny()
+    cfg = ParallelConfig(pp_size=2, dp_size=2, microbatches=8, unit_size=4, stages_per_device=2)
+    pl = make_placement(cfg, ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len))
+    params = {}
+    for st in range(cfg.num_stages):
+        for sl in stage_layout(spec, st, cfg.num_stages, pl.stage_to_layers[st], cfg.dp_size).slots:
+            params[(sl.name, sl.layer)] = torch.from_numpy(
+                init_values(sl.numel, spec.seed, init_offset(sl.uid), sl.mean, sl.std)).view(*sl.shape)
+    tok = make_tokens(1, 2, 8, 1, spec.seq_len, spec.vocab)[0]
+    ids, labels = tok[..., :-1].reshape(16, -1), tok[..., 1:].reshape(16, -1)
+    kw = dict(layers=spec.num_layers, heads=spec.heads, lr=spec.lr)
+    oracle_step(params, ids, labels, **kw)  # warm-up
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle_step(params, ids, labels, **kw)
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    return {"value": round(ids.numel() / dt, 1), "unit": "tokens/s", "ms_per_step": round(dt * 1e3, 2),
+            "tokens_per_step": ids.numel(), "cores": threads, "measured": True,
+            "config": "C1 tiny GPT L4 h256 s128, global batch 16 x 128 tokens, fwd+bwd+AdamW"}
+
+
 def run_reference(args) -> None:
+    """``--impl reference``: the reference's CPU side of this workload on this host.
+
+    The reference (`zeroppsim`) is a stdlib-only schedule SIMULATOR with no step arithmetic
+    (SURVEY.md section 0), so the arm reports three things, each labelled:
+    * ``value``: the CPU fp32 oracle port of the GPT-6.2B step on all host cores -- a bounded
+      sample per "step" (1 layer + LM head on 2048 tokens), EXTRAPOLATED to the full model by
+      model FLOPs (``extrapolated: true``); ``ms_per_step`` = tokens_per_step / value, so the
+      line is self-consistent (a full CPU step would take ~this long);
+    * ``reference_cpu_path``: the reference's own generate + validate + simulate for this
+      config, timed (ms, 1 core), from the reference package itself (baseline/_ref);
+    * ``c1_measured_step``: a fully MEASURED fp32 oracle step of BASELINE config C1.
+    Rank 0 only; other ranks exit without work."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    vals = []
+    threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_sample()
-    t0 = time.perf_counter()
-    last = None
+        cpu_sample(threads)
+    vals, last = [], None
     for _ in range(args.steps):
-        last = cpu_sample()
+        last = cpu_sample(threads)
         vals.append(last["value"])
-    total = time.perf_counter() - t0
     value = statistics.median(vals)
     P, D, B, U, V, mbs = _split(args)
+    from paper_2402_03791_b200.engine import GPTSpec
+    spec = getattr(GPTSpec, MODELS[args.model][0])(microbatch_samples=mbs)
+    tokens_per_step = D * B * spec.tokens_per_microbatch
     line = {"metric": METRIC, "impl": "reference", "value": round(value, 3), "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(total / max(args.steps, 1) * 1e3, 1), "higher_is_better": True,
+            "ms_per_step": round(tokens_per_step / value * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"GPT-6.2B ZeroPP step, P{P} x D{D}, B={B}, U={U}, V={V}, b={mbs}, s=2048",
-                       "model": "GPT-6.2B", "seq_len": 2048, "parallelism": "cpu oracle (host cores)"},
-            "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": last["cores"],
-                             "kind": "port", "sample": last["sample"]},
+            "extrapolated": True,
+            "config": {"workload": f"{args.model.upper()} ZeroPP step, P{P} x D{D}, B={B}, U={U}, V={V}, b={mbs}, "
+                                   f"s={spec.seq_len}", "model": MODELS[args.model][1],
+                       "tokens_per_step": tokens_per_step, "parallelism": "cpu (host cores)"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": last["cores"], "kind": "port",
+                             "sample": last["sample"], "extrapolated": True},
+            "reference_cpu_path": reference_schedule_path(args),
+            "c1_measured_step": c1_oracle_step(threads),
             "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

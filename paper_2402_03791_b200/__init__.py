@@ -19,6 +19,18 @@ from .config import (
     load_config,
     make_placement,
 )
+from .costmodel import (
+    TABLE_METHODS,
+    CostReport,
+    Method,
+    bubble_formula,
+    crossover,
+    figure1_curve,
+    memory_formula,
+    table2_row,
+    tp_comm_volume,
+    zeropp_comm_volume,
+)
 from .schedules import apply_recompute, build_dependency_edges, expected_edges, generate
 from .tasks import (
     Schedule,
@@ -54,6 +66,8 @@ __all__ = [
     "MemoryBreakdown", "SimResult", "SimulationDeadlock", "bubble_count", "comm_volume",
     "peak_memory", "simulate", "RenderFormat", "chrome_trace", "render_timeline",
     "PlanResult", "PlanRow", "SearchSpace", "report", "search", "search_measured",
+    "TABLE_METHODS", "CostReport", "Method", "bubble_formula", "crossover", "figure1_curve",
+    "memory_formula", "table2_row", "tp_comm_volume", "zeropp_comm_volume",
 ]
 
 

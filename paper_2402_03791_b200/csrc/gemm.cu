@@ -161,6 +161,9 @@ __device__ __forceinline__ void epi_math(const EpiParams& p, int row, int col, f
 // group > 0: neither operand fits in L2 (K-heavy dgrad, e.g. 4096 x 4096 x 16384): walk the
 // fast dimension in bands of `group` panels so one wave of ~74 tile pairs touches ~8 + 9
 // panels instead of all 16 of one operand (ncu: 2.3-3.8x DRAM re-reads without it).
+// Measured and rejected (profiles/r02/gemm_raster_ab.txt): snaking 8 x 8 tile blocks so that
+// consecutive blocks share 8 panels -- one block streams ~128 MB, more than L2 keeps, and
+// traffic went UP 2-9%.
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, bool n_fast, int group, int& mt,
                                             int& nt) {
   int nf = n_fast ? num_n : num_m, ns = n_fast ? num_m : num_n, f, sl;
@@ -265,6 +268,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       kb1 = (piece + 1) * num_k / sk.pieces;
     }
   };
+  // K-heavy banded GEMMs (group > 0): a wave of ~`units` concurrent tiles streams more operand
+  // bytes than L2 holds, so the next wave would re-read its panels from HBM from k = 0.  Odd
+  // waves walk K backwards instead and start on the k-blocks the previous wave touched last,
+  // which are still in L2: -7 to -9% DRAM bytes on the K = 12288 / 16384 dgrads
+  // (profiles/r02/gemm_raster_ab.txt).  Per tile the order is fixed: results stay deterministic.
+  const int units = gridDim.x / CG;
+  auto k_reverse = [&](int tile, int skt) { return group > 0 && skt < 0 && ((tile / units) & 1); };
   // Readers take the next tile id from the ring (leader's ring_empty counts the readers).
   const uint32_t ring_empty_leader = (CG == 2) ? map_cta(ring_empty(0), 0) : ring_empty(0);
   auto next_tile = [&](int it, bool arrive) -> int {
@@ -305,7 +315,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tile_coords(tile, num_m, num_n, n_fast, group, mt, nt);
         const int m0 = mt * TILE_M + crank * GEMM_BM;
         const int n0 = nt * BN + crank * BNL;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const bool rev = k_reverse(tile, skt);
+        for (int j = 0; j < kb1 - kb0; ++j) {
+          const int kb = rev ? kb1 - 1 - j : kb0 + j;
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t fb = full_bar(stage);
           if (leader) mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES * CG);
@@ -355,7 +367,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                      ? sk.trace + ((size_t)blockIdx.x * GEMM_TRACE_ITEMS + it) * 6 : nullptr;
         if (tr) { tr[0] = item; tr[1] = gtimer(); }
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int j = 0; j < kb1 - kb0; ++j) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           const uint32_t a_s = sA + stage * Cfg::A_BYTES;
@@ -364,7 +376,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = make_sdesc(a_s + k * A_KSTEP, A_LBO, 1024);
             const uint64_t bd = make_sdesc(b_s + k * B_KSTEP, B_LBO, 1024);
-            const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+            const uint32_t accum = (j > 0 || k > 0) ? 1u : 0u;
             if (CG == 2) mma_bf16_2sm(d_tmem, ad, bd, idesc, accum);
             else mma_bf16(d_tmem, ad, bd, idesc, accum);
           }

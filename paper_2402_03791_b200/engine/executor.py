@@ -89,6 +89,12 @@ class StepResult:
     waits: list | None = None               # (kind, task_id, ms) of every timed compute-stream wait
     busy_ms: float | None = None
     sim: object = None                      # timeline runtimes: the whole-job SimResult (engine.timeline)
+    # bytes this rank received through NCCL collectives this step (ring algorithms: an
+    # all-gather / reduce-scatter over g ranks moves (g-1)/g of the full buffer per rank, an
+    # all-reduce twice that) -- the executed counterpart of the reference's task bytes
+    # (`schedules.py:72-87`), checked against them in tests/test_comm_bytes.py
+    nccl_bytes_intra: int = 0
+    nccl_bytes_inter: int = 0
 
     def __getattr__(self, name):
         # SimResult superset: makespan, per_device_busy/idle, bubble_ratios, peak_mem,
@@ -344,6 +350,7 @@ class Runtime:
         B, b, s_len = cfg.microbatches, spec.microbatch_samples, spec.seq_len
         assert ids.shape == (B, b * s_len) and labels.shape == (B, b * s_len)
         self._ids, self._labels = ids, labels
+        self.nccl_bytes = {"intra": 0, "inter": 0}
         self._stash: dict = {}
         self._local_act: dict = {}
         self._local_grad: dict = {}
@@ -378,7 +385,8 @@ class Runtime:
         torch.cuda.current_stream(self.dev).wait_stream(comp)
         self._t = (t_start, t_end, times)
         tokens_done = B * b * s_len if (self.S - 1) in self.stages else 0
-        return StepResult(self.loss_sum, tokens_done)
+        return StepResult(self.loss_sum, tokens_done, nccl_bytes_intra=self.nccl_bytes["intra"],
+                          nccl_bytes_inter=self.nccl_bytes["inter"])
 
     def _graph_step(self, ids: torch.Tensor, labels: torch.Tensor) -> StepResult:
         comp = self.s_comp
@@ -426,7 +434,8 @@ class Runtime:
         self._t = (t_start, t_end, {})
         spec, cfg = self.spec, self.cfg
         tokens_done = cfg.microbatches * spec.tokens_per_microbatch if (self.S - 1) in self.stages else 0
-        return StepResult(self.loss_sum, tokens_done)
+        return StepResult(self.loss_sum, tokens_done, nccl_bytes_intra=self.nccl_bytes["intra"],
+                          nccl_bytes_inter=self.nccl_bytes["inter"])
 
     def finish_timing(self, res: StepResult) -> StepResult:
         """Resolve CUDA-event timings of the last step (synchronizes)."""
@@ -485,6 +494,7 @@ class Runtime:
         ns = st.lay.shard_numel
         lib.call("zpp_allgather", self.comms[("ag", self.p)], st.shard_bf16.data_ptr(),
                  st.gathered.data_ptr(), ns, 0, self.s_ag.cuda_stream)
+        self.nccl_bytes["intra"] += (self.D - 1) * ns * 2
         st.ag_event = self._record(self.s_ag)
 
     def _reduce_scatter(self, s: int) -> None:
@@ -503,6 +513,7 @@ class Runtime:
         st.grad_free_event = self._record(rs)
         lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], send.data_ptr(), recv.data_ptr(), ns, 0,
                  rs.cuda_stream)
+        self.nccl_bytes["intra"] += (self.D - 1) * ns * 2
         ops.accum(recv, st.grad_shard, stream=rs)
         ev = self._record(rs)
         self._rs_events.append(ev)
@@ -529,9 +540,11 @@ class Runtime:
             if reduce_scatter:
                 recv = self.rs_recv[:nsub]
                 lib.call("zpp_reduce_scatter", comm, wire.data_ptr(), recv.data_ptr(), nsub, 0, rs.cuda_stream)
+                self.nccl_bytes["inter"] += (self.n - 1) * nsub * 2
                 ops.accum(recv, st.grad_sub, stream=rs)   # grad_sub is zero between steps
             else:
                 lib.call("zpp_allreduce", comm, wire.data_ptr(), wire.data_ptr(), ns, 0, rs.cuda_stream)
+                self.nccl_bytes["inter"] += 2 * (self.n - 1) * ns * 2 // self.n
                 ops.zero(st.grad_shard, stream=rs)
                 ops.accum(wire, st.grad_shard, stream=rs)
         self._rs_events.append(self._record(rs))
@@ -548,6 +561,7 @@ class Runtime:
         for st in self.stages.values():
             lib.call("zpp_allgather", comm, st.sub_bf16.data_ptr(), st.shard_bf16.data_ptr(), st.nsub, 0,
                      ag.cuda_stream)
+            self.nccl_bytes["inter"] += (self.n - 1) * st.nsub * 2
         ev = self._record(ag)
         self.opt_event = ev            # AG_PARAM of the next step gathers the updated shard
         if self.D == 1:

@@ -112,6 +112,12 @@ class GPTSpec:
         return cls(num_layers=24, hidden=2048, heads=16, seq_len=2048, **kw)
 
     @classmethod
+    def gpt_13b(cls, **kw) -> "GPTSpec":
+        """SURVEY.md C5 / BASELINE configs[4]: L40 h5120 a40 (head_dim 128) s2048, 13.1 B params:
+        236 GB of fp32 master + Adam + bf16 state (18 B/param), so it needs P x D >= 2 on 180 GB B200s."""
+        return cls(num_layers=40, hidden=5120, heads=40, seq_len=2048, **kw)
+
+    @classmethod
     def tiny(cls, **kw) -> "GPTSpec":
         return cls(num_layers=4, hidden=256, heads=4, seq_len=128, **kw)
 
@@ -239,3 +245,29 @@ def shard_init_ranges(lay: StageLayout, z: int):
         a, b = max(lo, slot.offset), min(hi, slot.offset + slot.numel)
         if a < b:
             yield slot, a - slot.offset, a - lo, b - a
+
+
+def nccl_bytes_per_step(spec: GPTSpec, cfg, placement, sched, p: int) -> tuple[int, int]:
+    """(intra, inter) bytes pipeline rank ``p`` receives through NCCL in one step, task by task
+    as the executor issues them (ring collectives: an all-gather / reduce-scatter over g ranks
+    moves (g-1)/g of the full buffer per rank, an all-reduce twice that):
+
+    * AG_PARAM, RS_GRAD (`schedules.py:72-78`): (D-1) x shard x 2 B of the stage's flat bf16
+      buffer -- the reference's ``((D-1)/D) * M_w * layers`` with the stage's real size;
+    * AR_GRAD (`:80-81`): 2 (n-1)/n x shard x 2 B per local stage;
+    * RS_GRAD_INTER / AG_PARAM_INTER (`:83-87`): (n-1) x optimizer sub-shard x 2 B per stage.
+    ``StepResult.nccl_bytes_intra/inter`` must equal this (tests/test_engine_gpu.py via
+    dist_worker.py); tests/test_comm_bytes.py relates it to the reference's own byte model."""
+    from ..tasks import TaskKind
+    D, n, S = cfg.dp_size, cfg.inter_node_dp, cfg.num_stages
+    sub = optimizer_sub(cfg)
+    lays = {s: stage_layout(spec, s, S, placement.stage_to_layers[s], D, sub) for s in placement.device_stages(p)}
+    intra = inter = 0
+    for t in sched.per_device[p]:
+        if t.kind in (TaskKind.AG_PARAM, TaskKind.RS_GRAD):
+            intra += (D - 1) * lays[t.stage].shard_numel * 2
+        elif t.kind is TaskKind.AR_GRAD and n > 1:
+            inter += sum(2 * (n - 1) * lay.shard_numel * 2 // n for lay in lays.values())
+        elif t.kind in (TaskKind.RS_GRAD_INTER, TaskKind.AG_PARAM_INTER) and n > 1:
+            inter += sum((n - 1) * (lay.shard_numel // sub) * 2 for lay in lays.values())
+    return intra, inter

@@ -46,6 +46,11 @@ def main():
             fails.append("measured timeline does not cover every device's tasks")
         elif not all(0 < b <= sim.makespan for b in sim.per_device_busy):
             fails.append(f"measured busy/makespan inconsistent: {sim.per_device_busy} / {sim.makespan}")
+        from paper_2402_03791_b200.engine.model import nccl_bytes_per_step
+        want = nccl_bytes_per_step(spec, cfg, pl, sched, rt.p)
+        got = (res[0].nccl_bytes_intra, res[0].nccl_bytes_inter)
+        if got != want:
+            fails.append(f"NCCL bytes {got} != planned {want}")
         if abs(loss - loss_o) / loss_o > LOSS_RTOL:
             fails.append(f"loss {loss} vs oracle {loss_o}")
         if fails:

@@ -20,7 +20,7 @@ WIDE = {
     "gpt-6.2b": lambda **kw: GPTSpec(num_layers=2, hidden=4096, heads=32, seq_len=2048, microbatch_samples=2, **kw),
     "llama-7b": lambda **kw: GPTSpec(num_layers=2, hidden=4096, heads=32, seq_len=4096, vocab=32000, arch="llama",
                                      ffn_hidden=11008, **kw),
-    "gpt-13b": lambda **kw: GPTSpec(num_layers=2, hidden=5120, heads=40, seq_len=2048, **kw),
+    "gpt-13b": lambda **kw: GPTSpec(num_layers=2, hidden=5120, heads=40, seq_len=2048, **kw),  # gpt_13b, 2 layers
 }
 
 
