@@ -172,9 +172,14 @@ def run_zpp(args) -> None:
     sched = generate(model, cfg, pl)
     rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=True)
     z = rt.z
-    toks = make_tokens(1, D, B, mbs, spec.seq_len, spec.vocab)[0]
-    ids_h = toks[z, :, :, :-1].reshape(B, -1).contiguous().pin_memory()
-    lab_h = toks[z, :, :, 1:].reshape(B, -1).contiguous().pin_memory()
+    # NB distinct synthetic batches, cycled step by step: a repeated batch would be memorised
+    # within a few steps (loss -> 0), which is not a training workload
+    NB = 4
+    toks = make_tokens(NB, D, B, mbs, spec.seq_len, spec.vocab)
+    ids_hs = [toks[k, z, :, :, :-1].reshape(B, -1).contiguous().pin_memory() for k in range(NB)]
+    lab_hs = [toks[k, z, :, :, 1:].reshape(B, -1).contiguous().pin_memory() for k in range(NB)]
+    ids_ds, lab_ds = [x.cuda() for x in ids_hs], [x.cuda() for x in lab_hs]
+    ids_h, lab_h = ids_hs[0], lab_hs[0]
     ids_d, lab_d = ids_h.cuda(), lab_h.cuda()
     tokens_per_step = D * B * spec.tokens_per_microbatch
 
@@ -191,8 +196,8 @@ def run_zpp(args) -> None:
         return t.item()
 
     # warm-up (also lets the caching allocator settle)
-    for _ in range(args.warmup):
-        rt.step(ids_d, lab_d)
+    for k in range(args.warmup):
+        rt.step(ids_ds[k % NB], lab_ds[k % NB])
     barrier()
 
     # ---- kernel-resident timed region (value) ----------------------------------
@@ -203,8 +208,8 @@ def run_zpp(args) -> None:
     barrier()
     ev0.record(comp)
     results = []
-    for _ in range(args.steps):
-        results.append(rt.step(ids_d, lab_d))
+    for k in range(args.steps):
+        results.append(rt.step(ids_ds[k % NB], lab_ds[k % NB]))
     ev1.record(comp)
     barrier()
     launches = ops.PROFILE.launches
@@ -215,8 +220,8 @@ def run_zpp(args) -> None:
     graph_mode, rt.graph_mode = rt.graph_mode, False  # per-GEMM events need eager launches
     ops.PROFILE.start(time_gemms=True)
     barrier()
-    for _ in range(args.steps):
-        rt.step(ids_d, lab_d)
+    for k in range(args.steps):
+        rt.step(ids_ds[k % NB], lab_ds[k % NB])
     barrier()
     gemm_flops, gemm_ms, gemm_calls = ops.PROFILE.stop()
     rt.graph_mode = graph_mode
@@ -238,9 +243,9 @@ def run_zpp(args) -> None:
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        ids_d.copy_(ids_h, non_blocking=True)
-        lab_d.copy_(lab_h, non_blocking=True)
+    for k in range(args.steps):
+        ids_d.copy_(ids_hs[k % NB], non_blocking=True)
+        lab_d.copy_(lab_hs[k % NB], non_blocking=True)
         r = execute(sched, model, cfg, pl, rt, ids_d, lab_d)
         _ = r.loss_sum.item()
     e1.record()
@@ -260,7 +265,7 @@ def run_zpp(args) -> None:
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (seeded CPU randint tokens, deterministic counter-hash init)",
+            "data": "synthetic (seeded CPU randint tokens, 4 distinct batches cycled; deterministic counter-hash init)",
             "config": {"workload": f"{args.model.upper()} ZeroPP step, P{P} x D{D}, B={B} micro-batches/ZeRO "
                                    f"rank, U={U}, V={V}, b={mbs}, s={spec.seq_len}",
                        "model": MODELS[args.model][1],

@@ -82,6 +82,25 @@ __device__ __forceinline__ void store_acc_row(uint32_t tacc, uint32_t lo, int hh
                      pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
   }
 }
+// Thread = TMEM lane r of a 128-row accumulator, quarter `part` of its D columns -> bf16.
+template <int D>
+__device__ __forceinline__ void store_acc_quarter(uint32_t tacc, uint32_t lo, int part, bf16* dst) {
+  constexpr int W = D / 4;  // 32 or 16 columns
+  uint32_t v[32];
+  if constexpr (W == 32) {
+    tmem_ld32(tacc + lo + part * 32, v);
+  } else {
+    tmem_ld16(tacc + lo + part * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
+  }
+  tmem_wait_ld();
+#pragma unroll
+  for (int k = 0; k < W; k += 8)
+    *reinterpret_cast<uint4*>(dst + part * W + k) =
+        make_uint4(pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                   pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
+                   pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
+                   pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
@@ -131,6 +150,9 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 128) ZTRACE(0, 0, 63);
+  // programmatic dependent launch: once every dQ CTA is resident, dK/dV CTAs may take the SMs
+  // the dQ tail frees (they wait for our delta / lse2 with griddepcontrol.wait)
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // 1-D grid, heaviest query blocks first across ALL heads
   const int nqb = T / 128;
   const int bh = blockIdx.x % BH, b = bh / H, h = bh % H;
@@ -367,33 +389,37 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// dK / dV.  warp 0: TMA K, V once, then Q_t / dO_t (+ lse2_t, delta_t) through a ring of 4;
-// warp 1: MMA issuer; warp 2: TMEM owner; warps 4..11: thread = key row (TMEM lane), warp
-// (quarter q, half hh) takes queries [32hh, 32hh+32) of each 64-query tile.
-// TMEM: dV [0,D), dK [D,2D), S^T/P^T [2D,2D+128) (2 x 64), dP^T [2D+128, 2D+256) (2 x 64).
+// dK / dV.  warp 0: TMA K, V once, then Q_t / dO_t (+ lse2_t, delta_t) through a ring of 3;
+// warp 1: MMA issuer; warp 2: TMEM owner; warps 4..19: thread = key row (TMEM lane), warp
+// (quarter q, part) takes queries [16 part, 16 part + 16) of each 64-query tile.
+// K and V are copied into TMEM once (the A operands of S^T / dP^T: TS-mode MMAs run at the
+// tensor core's rate for N = 64, the SS form is bound by re-reading the 128-row A from smem).
+// S^T / dP^T are single-buffered but released as soon as the row threads have loaded them,
+// so S^T(t+1), dP^T(t+1) run while the exp2 phase of tile t does; P^T and dS^T go to smem
+// (the A operands of dV += P^T dO and dK += dS^T Q, N = d = 128: full rate from smem).
+// TMEM: dV [0,D) dK [D,2D) K [2D,2D+D/2) V [2D+D/2,3D) S^T [3D,3D+64) dP^T [3D+64,3D+128).
 template <int D>
 struct BwdDkdvCfg {
   static constexpr int KATOM = 128 * 128;  // [128 rows][64 bf16]
   static constexpr int KTILE = (D / 64) * KATOM;
   static constexpr int QATOM = 64 * 128;   // [64 rows][64 bf16]
   static constexpr int QTILE = (D / 64) * QATOM;
-  // ring of 4: the Q/dO stage of tile t+4 frees when dK(t) retires, two tiles before S^T(t+4)
-  // is issued -- one tile (~0.5 us at the tensor core's rate) does not hide an L2 TMA round trip
-  static constexpr int QST = 4;
-  static constexpr int DS_BYTES = 128 * 128;  // dS^T [128 keys][64 queries] bf16 (one buffer)
+  static constexpr int QST = 3;
+  static constexpr int PT_BYTES = 128 * 128;  // P^T or dS^T: [128 keys][64 queries] bf16
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + KTILE;
   static constexpr int Q_OFF = V_OFF + KTILE;
   static constexpr int DO_OFF = Q_OFF + QST * QTILE;
-  static constexpr int DS_OFF = DO_OFF + QST * QTILE;
-  static constexpr int L_OFF = DS_OFF + DS_BYTES;  // per stage: lse2 [64] | delta [64]
+  static constexpr int PT_OFF = DO_OFF + QST * QTILE;
+  static constexpr int DS_OFF = PT_OFF + PT_BYTES;
+  static constexpr int L_OFF = DS_OFF + PT_BYTES;  // per stage: lse2 [64] | delta [64]
   static constexpr int BAR_OFF = L_OFF + QST * 512;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "smem budget");
 };
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(640, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse2,
                          const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, int BH,
@@ -406,8 +432,8 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t bars = base + C::BAR_OFF;
   const uint32_t kv_full = bars, qd_full0 = bars + 8, qd_empty0 = qd_full0 + 8 * C::QST;
-  const uint32_t sp_full0 = qd_empty0 + 8 * C::QST, ds_full0 = sp_full0 + 16, ds_free = ds_full0 + 16;
-  const uint32_t mm_done = ds_free + 8;
+  const uint32_t kv_tmem = qd_empty0 + 8 * C::QST, sp_full = kv_tmem + 8, sp_free = sp_full + 8;
+  const uint32_t ds_full = sp_free + 8, ds_free = ds_full + 8, mm_done = ds_free + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -427,10 +453,10 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(qd_full0 + 8 * s, 1);
       mbar_init(qd_empty0 + 8 * s, 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(sp_full0 + 8 * s, 1);
-      mbar_init(ds_full0 + 8 * s, 256);
-    }
+    mbar_init(kv_tmem, 512);
+    mbar_init(sp_full, 1);
+    mbar_init(sp_free, 512);
+    mbar_init(ds_full, 512);
     mbar_init(ds_free, 1);
     mbar_init(mm_done, 1);
     fence_mbar_init();
@@ -440,7 +466,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t T_DV = tmem, T_DK = tmem + D, T_S = tmem + 2 * D, T_DP = tmem + 2 * D + 128;
+  const uint32_t T_DV = tmem, T_DK = tmem + D, T_K = tmem + 2 * D, T_V = T_K + D / 2, T_S = tmem + 3 * D,
+                 T_DP = T_S + 64;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -459,6 +486,7 @@ __global__ void __launch_bounds__(384, 1)
           tma_load_2d(base + C::Q_OFF + st * C::QTILE + a * C::QATOM, &tm_q, fb, h * D + 64 * a, row_base + q0);
           tma_load_2d(base + C::DO_OFF + st * C::QTILE + a * C::QATOM, &tm_do, fb, h * D + 64 * a, row_base + q0);
         }
+        if (it == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // delta / lse2 of the dQ kernel
         bulk_load_1d(base + C::L_OFF + st * 512, lse2 + (long long)bh * T + q0, 256, fb);
         bulk_load_1d(base + C::L_OFF + st * 512 + 256, delta + (long long)bh * T + q0, 256, fb);
       }
@@ -468,114 +496,149 @@ __global__ void __launch_bounds__(384, 1)
     {  // whole warp: uniform descriptors, elect.sync issues
       constexpr uint32_t id_sp = make_idesc_bf16(128, 64, false, false);  // S^T, dP^T: N = 64 queries
       constexpr uint32_t id_kv = make_idesc_bf16(128, D, false, true);    // dV, dK: B N-major (N = d)
-      mbar_wait(kv_full, 0);
-      auto issue_sp = [&](int it) {
+      auto issue_sp = [&](int it) {  // S^T = K Q^T, dP^T = V dO^T (A = K / V from TMEM)
         const int st = it % C::QST;
         mbar_wait(qd_full0 + 8 * st, (it / C::QST) & 1);
         tc_fence_after();
         const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
-        const uint32_t buf = (it & 1) * 64;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_w(T_S + buf, make_sdesc(base + C::K_OFF + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024),
-                   make_sdesc(qs + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024), id_sp, kk > 0 ? 1u : 0u);
+          mma_bf16_ts_w(T_S, T_K + kk * 8, make_sdesc(qs + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024), id_sp,
+                        kk > 0 ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_w(T_DP + buf, make_sdesc(base + C::V_OFF + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024),
-                   make_sdesc(dos + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024), id_sp, kk > 0 ? 1u : 0u);
-        mma_commit_w(sp_full0 + 8 * (it & 1));
+          mma_bf16_ts_w(T_DP, T_V + kk * 8, make_sdesc(dos + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024),
+                        id_sp, kk > 0 ? 1u : 0u);
+        mma_commit_w(sp_full);
       };
+      mbar_wait(kv_tmem, 0);  // K, V copied into TMEM by the row threads
+      tc_fence_after();
       issue_sp(0);
-      if (nq > 1) issue_sp(1);
       for (int it = 0; it < nq; ++it) {
         const int st = it % C::QST;
         const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+        if (it + 1 < nq) {
+          mbar_wait(sp_free, it & 1);  // the row threads have loaded S^T(it), dP^T(it)
+          tc_fence_after();
+          issue_sp(it + 1);
+        }
         ZTRACE(1, 0, it);
-        mbar_wait(ds_full0 + 8 * (it & 1), (it >> 1) & 1);
+        mbar_wait(ds_full, it & 1);
         ZTRACE(1, 1, it);
         tc_fence_after();
         const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO: A = P^T (TMEM, each 32-query half in its first 16 cols)
-          mma_bf16_ts_w(T_DV, T_S + (it & 1) * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
-                      make_sdesc(dos + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO: A = P^T (smem K-major), B = dO (N-major)
+          mma_bf16_w(T_DV, make_sdesc(base + C::PT_OFF + kk * 32, 16, 1024), make_sdesc(dos + kk * 2048, C::QATOM, 1024),
+                     id_kv, (acc0 | kk) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q: A = dS^T (smem K-major), B = Q (N-major)
-          mma_bf16_w(T_DK, make_sdesc(base + C::DS_OFF + kk * 32, 16, 1024),
-                   make_sdesc(qs + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
+          mma_bf16_w(T_DK, make_sdesc(base + C::DS_OFF + kk * 32, 16, 1024), make_sdesc(qs + kk * 2048, C::QATOM, 1024),
+                     id_kv, (acc0 | kk) ? 1u : 0u);
         mma_commit_w(ds_free);
         mma_commit_w(qd_empty0 + 8 * st);
         ZTRACE(1, 2, it);
-        if (it + 2 < nq) issue_sp(it + 2);  // S^T over P^T(it) after dV read it (in-order pipe)
-        ZTRACE(1, 3, it);
       }
       mma_commit_w(mm_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
+    // 16 row warps (4 per SM sub-partition): warp (quarter q, part) owns key rows 32q..32q+31
+    // and queries [16 part, 16 part + 16) of each tile -- enough warps in flight to hide the
+    // TMEM-load -> exp2 -> smem-store latency chain (with 8 warps the exp2 phase, not the
+    // tensor core, set the pace: ~1000 cycles per tile vs ~1024 of MMA work)
     const int q = warp & 3;
-    const int hh = (warp - 4) >> 2;
+    const int part = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // key row == TMEM lane
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * kLog2e;
+    {  // K and V rows -> TMEM (this thread: key row r, quarter `part` of the D columns)
+      constexpr int CH = D / 32;  // 16-byte chunks per quarter row
+      uint32_t kv[4 * CH], vv[4 * CH];
+      mbar_wait(kv_full, 0);
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int cg = part * CH + i;
+        const uint32_t off = (cg >> 3) * C::KATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
+        const uint4 k4 = ld_shared_v4(base + C::K_OFF + off), v4 = ld_shared_v4(base + C::V_OFF + off);
+        kv[4 * i] = k4.x, kv[4 * i + 1] = k4.y, kv[4 * i + 2] = k4.z, kv[4 * i + 3] = k4.w;
+        vv[4 * i] = v4.x, vv[4 * i + 1] = v4.y, vv[4 * i + 2] = v4.z, vv[4 * i + 3] = v4.w;
+      }
+      if constexpr (CH == 4) {
+        tmem_st16(T_K + lo + part * 16, kv);
+        tmem_st16(T_V + lo + part * 16, vv);
+      } else {
+        tmem_st8(T_K + lo + part * 8, kv);
+        tmem_st8(T_V + lo + part * 8, vv);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(kv_tmem);
+    }
     for (int it = 0; it < nq; ++it) {
-      const int buf = it & 1;
-      const uint32_t par = (it >> 1) & 1;
-      const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (it % C::QST) * 512) + hh * 32;
+      const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (it % C::QST) * 512) + part * 16;
       if (threadIdx.x == 128) ZTRACE(1, 4, it);
-      mbar_wait(sp_full0 + 8 * buf, par);
+      mbar_wait(sp_full, it & 1);
       if (threadIdx.x == 128) ZTRACE(1, 5, it);
       tc_fence_after();
-      uint32_t sv[32], pv[32];
-      tmem_ld32(T_S + lo + buf * 64 + hh * 32, sv);
-      tmem_ld32(T_DP + lo + buf * 64 + hh * 32, pv);
+#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (row threads only hand over)
+      tc_fence_before();
+      mbar_arrive(sp_free);
+      if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);
+      mbar_arrive(ds_full);
+      if (threadIdx.x == 128) ZTRACE(1, 7, it);
+      continue;
+#endif
+      uint32_t sv[16], pv[16];
+      tmem_ld16(T_S + lo + part * 16, sv);
+      tmem_ld16(T_DP + lo + part * 16, pv);
       tmem_wait_ld();
-      float p[32], ds[32];
+      tc_fence_before();
+      mbar_arrive(sp_free);  // S^T(it+1) / dP^T(it+1) may now overwrite the buffers
+      float p[16], ds[16];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < 16; j += 4) {
         const float4 l4 = *reinterpret_cast<const float4*>(L + j);
         const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + j);
         const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           p[j + u] = fast_exp2(fmaf(__uint_as_float(sv[j + u]), sl2, -lv[u]));
-          ds[j + u] = dv[u];
+          ds[j + u] = dv[u] * scale;
         }
       }
       if (it < 2) {  // tiles on the diagonal: key after query
-        const int qk = it * 64 + hh * 32 - r;
+        const int qk = it * 64 + part * 16 - r;
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
+        for (int j = 0; j < 16; ++j)
           if (qk + j < 0) p[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) ds[j] = p[j] * (__uint_as_float(pv[j]) - ds[j]) * scale;
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
-      tmem_st16(T_S + lo + buf * 64 + hh * 32, pk);  // P^T over S^T columns this warp has read
+      for (int j = 0; j < 16; ++j) ds[j] = p[j] * fmaf(__uint_as_float(pv[j]), scale, -ds[j]);
       if (threadIdx.x == 128) ZTRACE(1, 6, it);
-      if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);  // dK(it-1) done reading dS^T
-      const uint32_t rowp = base + C::DS_OFF + r * 128;
+      if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);  // dV / dK(it-1) done reading P^T / dS^T
+      const uint32_t rp = base + C::PT_OFF + r * 128, rd = base + C::DS_OFF + r * 128;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int c8 = hh * 4 + t;
-        const float* s = &ds[t * 8];
-        st_shared_v4(rowp + ((c8 ^ (r & 7)) << 4), pack_bf16(s[0], s[1]), pack_bf16(s[2], s[3]),
-                     pack_bf16(s[4], s[5]), pack_bf16(s[6], s[7]));
+      for (int t = 0; t < 2; ++t) {
+        const int c8 = part * 2 + t;
+        const float* pp = &p[t * 8];
+        const float* sd = &ds[t * 8];
+        const uint32_t sw = (c8 ^ (r & 7)) << 4;
+        st_shared_v4(rp + sw, pack_bf16(pp[0], pp[1]), pack_bf16(pp[2], pp[3]), pack_bf16(pp[4], pp[5]),
+                     pack_bf16(pp[6], pp[7]));
+        st_shared_v4(rd + sw, pack_bf16(sd[0], sd[1]), pack_bf16(sd[2], sd[3]), pack_bf16(sd[4], sd[5]),
+                     pack_bf16(sd[6], sd[7]));
       }
-      tmem_wait_st();
       fence_proxy_async();
-      tc_fence_before();
-      mbar_arrive(ds_full0 + 8 * buf);
+      mbar_arrive(ds_full);
       if (threadIdx.x == 128) ZTRACE(1, 7, it);
     }
     mbar_wait(mm_done, 0);
     if (threadIdx.x == 128) ZTRACE(1, 4, 63);
     tc_fence_after();
     bf16* dk = dqkv + ((long long)row_base + k0 + r) * 3 * H * D + (long long)H * D + (long long)h * D;
-    store_acc_row<D>(T_DK, lo, hh, dk);
-    store_acc_row<D>(T_DV, lo, hh, dk + (long long)H * D);
+    store_acc_quarter<D>(T_DK, lo, part, dk);
+    store_acc_quarter<D>(T_DV, lo, part, dk + (long long)H * D);
     if (threadIdx.x == 128) ZTRACE(1, 5, 63);
   }
   tc_fence_before();
@@ -633,8 +696,21 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
                                                                (bf16*)dqkv, T, H, BH, scale);
   rc = check_launch("attn_bwd_dq");
   if (rc) return rc;
-  attn_bwd_dkdv_kernel<D><<<grid, 384, BwdDkdvCfg<D>::SMEM, s>>>(m_kv128, m_q64, m_do64, lse2, delta, (bf16*)dqkv,
-                                                                   T, H, BH, scale);
+  // dK/dV launched as a programmatic dependent of the dQ kernel: its prologue (TMEM, barriers,
+  // K/V/Q/dO loads) runs on SMs the dQ tail leaves idle; only the lse2 / delta loads wait
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(640);
+  cfg.dynamicSmemBytes = BwdDkdvCfg<D>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, (const float*)lse2,
+                                     (const float*)delta, (bf16*)dqkv, T, H, BH, scale);
+  if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv launch");
   return check_launch("attn_bwd_dkdv");
 }
 

@@ -106,5 +106,6 @@ def test_costs_follow_layer_counts():
 
 
 def test_classic_baselines_are_out_of_scope():
-    with pytest.raises(NotImplementedError):
+    from paper_2402_03791_b200 import ConfigError
+    with pytest.raises(ConfigError, match="outside the engine's hot path"):
         build(mk_model(layers=4), mk_cfg(P=4, D=1, B=8, U=8), ScheduleVariant.GPIPE)
