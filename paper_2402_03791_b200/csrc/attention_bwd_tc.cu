@@ -65,6 +65,15 @@ __device__ __forceinline__ float dot8(uint4 a, uint4 b) {
   return fmaf(bf16hi(a.w), bf16hi(b.w), s);
 }
 
+// One arrival per warp on an mbarrier initialised with the number of arriving warps: a
+// 256/512-thread barrier takes every lane's arrive as a serialised shared-memory atomic, which
+// cost ~200 cycles of tensor-core idle per tile (measured).  Each lane's own prior TMEM
+// accesses are complete (tcgen05.wait::*) and its smem stores fenced before the __syncwarp.
+__device__ __forceinline__ void warp_arrive(uint32_t bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
 // Thread = TMEM lane r of a 128-row accumulator, half hh of its D columns -> bf16 row segment.
 template <int D>
 __device__ __forceinline__ void store_acc_row(uint32_t tacc, uint32_t lo, int hh, bf16* dst) {
@@ -177,10 +186,10 @@ __global__ void __launch_bounds__(384, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(s_full0 + 8 * s, 1);
       mbar_init(dp_full0 + 8 * s, 1);
-      mbar_init(ds_full0 + 8 * s, 256);
+      mbar_init(ds_full0 + 8 * s, 8);  // one arrival per row warp
     }
     mbar_init(dq_done, 1);
-    mbar_init(qt_full, 256);
+    mbar_init(qt_full, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(qt_full);
+      warp_arrive(qt_full);
     }
     red[hh * 128 + r] = acc;
     named_bar_sync(1, 256);
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(s_full0 + 8 * buf, par);
       mbar_wait(dp_full0 + 8 * buf, par);
       tc_fence_before();
-      mbar_arrive(ds_full0 + 8 * buf);
+      warp_arrive(ds_full0 + 8 * buf);
       if (threadIdx.x == 128) ZTRACE(0, 7, j);
       continue;
 #endif
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_st16(ts, pk);  // over S columns this warp has already read
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(ds_full0 + 8 * buf);
+      warp_arrive(ds_full0 + 8 * buf);
       if (threadIdx.x == 128) ZTRACE(0, 7, j);
     }
     mbar_wait(dq_done, 0);
@@ -453,10 +462,10 @@ __global__ void __launch_bounds__(640, 1)
       mbar_init(qd_full0 + 8 * s, 1);
       mbar_init(qd_empty0 + 8 * s, 1);
     }
-    mbar_init(kv_tmem, 512);
+    mbar_init(kv_tmem, 16);  // one arrival per row warp
     mbar_init(sp_full, 1);
-    mbar_init(sp_free, 512);
-    mbar_init(ds_full, 512);
+    mbar_init(sp_free, 16);
+    mbar_init(ds_full, 16);
     mbar_init(ds_free, 1);
     mbar_init(mm_done, 1);
     fence_mbar_init();
@@ -573,7 +582,7 @@ __global__ void __launch_bounds__(640, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(kv_tmem);
+      warp_arrive(kv_tmem);
     }
     for (int it = 0; it < nq; ++it) {
       const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (it % C::QST) * 512) + part * 16;
@@ -583,9 +592,9 @@ __global__ void __launch_bounds__(640, 1)
       tc_fence_after();
 #ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (row threads only hand over)
       tc_fence_before();
-      mbar_arrive(sp_free);
+      warp_arrive(sp_free);
       if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);
-      mbar_arrive(ds_full);
+      warp_arrive(ds_full);
       if (threadIdx.x == 128) ZTRACE(1, 7, it);
       continue;
 #endif
@@ -594,7 +603,7 @@ __global__ void __launch_bounds__(640, 1)
       tmem_ld16(T_DP + lo + part * 16, pv);
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(sp_free);  // S^T(it+1) / dP^T(it+1) may now overwrite the buffers
+      warp_arrive(sp_free);  // S^T(it+1) / dP^T(it+1) may now overwrite the buffers
       float p[16], ds[16];
 #pragma unroll
       for (int j = 0; j < 16; j += 4) {
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(640, 1)
                      pack_bf16(sd[6], sd[7]));
       }
       fence_proxy_async();
-      mbar_arrive(ds_full);
+      warp_arrive(ds_full);
       if (threadIdx.x == 128) ZTRACE(1, 7, it);
     }
     mbar_wait(mm_done, 0);

@@ -120,6 +120,140 @@ void run(const char* name) {
          double(cyc) / (iters * 4), macs_per_sm / cyc, 2.0 * macs_per_sm * 148 / (ms * 1e-3) / 1e12);
 }
 
+
+// the dK/dV kernel's per-tile MMA mix: S^T, dP^T (TS, N=64, K=128) + dV, dK (SS, N=128, K=64)
+template <int SYNC>
+__global__ void __launch_bounds__(128, 1) mma_mix(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, cb[4], done;
+  __shared__ uint32_t tslot;
+  const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&cb[i]), 1 << 20);  // never completes: commits only
+    mbar_init(smem_u32(&done), 1);
+    mbar_arrive(smem_u32(&done));  // phase 0 complete: waits on it return at once
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tslot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  auto sync_point = [&](int k) {
+    if (SYNC >= 1) mma_commit_w(smem_u32(&cb[k]));
+    if (SYNC >= 2) { mbar_wait(smem_u32(&done), 0); tc_fence_after(); }
+  };
+  if (warp == 0) {
+    constexpr uint32_t id_sp = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t id_kv = make_idesc_bf16(128, 128, false, true);
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_ts_w(tmem + 384, tmem + 256 + kk * 8, make_sdesc(base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                      id_sp, kk > 0);
+      sync_point(0);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_ts_w(tmem + 448, tmem + 320 + kk * 8, make_sdesc(base + 16384 + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                      id_sp, kk > 0);
+      sync_point(1);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16_w(tmem, make_sdesc(base + 32768 + kk * 32, 16, 1024), make_sdesc(base + kk * 2048, 8192, 1024), id_kv, 1);
+      sync_point(2);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16_w(tmem + 128, make_sdesc(base + 49152 + kk * 32, 16, 1024), make_sdesc(base + 16384 + kk * 2048, 8192, 1024),
+                   id_kv, 1);
+      sync_point(3);
+    }
+    mma_commit_w(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    unsigned long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int SYNC>
+void run_mix() {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  cudaFuncSetAttribute(mma_mix<SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  const int iters = 512;
+  mma_mix<SYNC><<<148, 128, 96 * 1024>>>(16, d);
+  mma_mix<SYNC><<<148, 128, 96 * 1024>>>(iters, d);
+  cudaError_t err = cudaDeviceSynchronize();
+  unsigned long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  printf("dkdv tile mix (16 TS N64 + 8 SS N128), sync %d  %s  %.1f cycles/tile (floor 1024)\n", SYNC,
+         cudaGetErrorString(err), double(cyc) / iters);
+}
+
+
+// dQ-kernel round: dQ += dS K (TS, A = TMEM buffer X, N=128, 4 x K16), then S = Q K^T and
+// dP = dO V^T (TS, N=64, 8 x K16 each) written into buffer Y.  WAR = Y is the buffer dQ read.
+template <bool WAR>
+__global__ void __launch_bounds__(128, 1) mma_dq_round(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc(smem_u32(&tslot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp == 0) {
+    constexpr uint32_t id_s = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t id_q = make_idesc_bf16(128, 128, false, true);
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t x = (i & 1) * 64;                       // dS buffer read by dQ
+      const uint32_t y = WAR ? x : ((i + 1) & 1) * 64;       // buffer S / dP are written into
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16_ts_w(tmem + 256, tmem + x + (kk >> 1) * 32 + (kk & 1) * 8, make_sdesc(base + kk * 2048, 8192, 1024),
+                      id_q, 1);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_ts_w(tmem + y, tmem + 384 + kk * 8, make_sdesc(base + 16384 + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                      id_s, kk > 0);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_ts_w(tmem + 128 + y, tmem + 448 + kk * 8,
+                      make_sdesc(base + 32768 + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+    }
+    mma_commit_w(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    unsigned long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <bool WAR>
+void run_dq_round() {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  cudaFuncSetAttribute(mma_dq_round<WAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  const int iters = 512;
+  mma_dq_round<WAR><<<148, 128, 96 * 1024>>>(16, d);
+  mma_dq_round<WAR><<<148, 128, 96 * 1024>>>(iters, d);
+  cudaError_t err = cudaDeviceSynchronize();
+  unsigned long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  printf("dq round (4 TS N128 + 16 TS N64), S/dP over the dS buffer dQ just read: %d  %s  %.1f cycles (floor 768)\n",
+         (int)WAR, cudaGetErrorString(err), double(cyc) / iters);
+}
+
 int main() {
   run<2, 256, 1, false, false>("cta2 K/K");
   run<2, 256, 1, false, true>("cta2 K/MN");
@@ -137,5 +271,8 @@ int main() {
   run_w<64, true>("warp N64 TS");
   run_w<32, false>("warp N32 SS");
   run_w<128, false>("warp N128 SS");
+  run_mix<0>();
+  run_dq_round<false>();
+  run_dq_round<true>();
   return 0;
 }
