@@ -29,6 +29,8 @@ import json
 import os
 
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # see zpp_preload_kernels
+if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+    os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line (no "NCCL version" banner)
 import statistics
 import subprocess
 import sys
