@@ -604,15 +604,17 @@ __global__ void __launch_bounds__(640, 1)
       tmem_wait_ld();
       tc_fence_before();
       warp_arrive(sp_free);  // S^T(it+1) / dP^T(it+1) may now overwrite the buffers
-      // this warp's 16 lse2 and 16 delta values: one 128-byte wavefront (lane l < 16 holds
-      // lse2, lane l >= 16 delta) and register shuffles, instead of 16 broadcast LDS.128 per
-      // warp -- shared memory is this kernel's bottleneck
-      const float lval = L[(lane < 16) ? lane : 64 + lane - 16];
       float p[16], ds[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        p[j] = fast_exp2(fmaf(__uint_as_float(sv[j]), sl2, -__shfl_sync(0xffffffffu, lval, j)));
-        ds[j] = __shfl_sync(0xffffffffu, lval, 16 + j) * scale;
+      for (int j = 0; j < 16; j += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(L + j);
+        const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + j);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          p[j + u] = fast_exp2(fmaf(__uint_as_float(sv[j + u]), sl2, -lv[u]));
+          ds[j + u] = dv[u] * scale;
+        }
       }
       if (it < 2) {  // tiles on the diagonal: key after query
         const int qk = it * 64 + part * 16 - r;
