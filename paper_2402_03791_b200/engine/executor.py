@@ -36,7 +36,7 @@ from ..config import HybridMode, ModelSpec, ParallelConfig, Placement, Recompute
 from ..tasks import Schedule, Task, TaskKind
 from ..validation import validate
 from . import lib, ops
-from .model import GPTSpec, StageLayout, init_offset, optimizer_sub, shard_init_ranges, stage_layout
+from .model import GPTSpec, StageLayout, init_offset, memory_estimate, optimizer_sub, shard_init_ranges, stage_layout
 
 BF16, F32 = torch.bfloat16, torch.float32
 
@@ -187,11 +187,12 @@ class Runtime:
     def __init__(self, spec: GPTSpec, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
-                 aux_stream: bool = True, host_trace: bool = False):
+                 aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
-        (first two steps, debugging)."""
+        (first two steps, debugging); ``memory_check``: refuse configurations whose estimated
+        peak does not fit (see below)."""
         if world != cfg.pp_size * cfg.dp_size * cfg.inter_node_dp:
             raise ValueError(f"world size {world} != n*P*D = "
                              f"{cfg.inter_node_dp * cfg.pp_size * cfg.dp_size}")
@@ -215,6 +216,16 @@ class Runtime:
             device = torch.cuda.current_device()
         self.dev = torch.device("cuda", device)
         torch.cuda.set_device(self.dev)
+        if memory_check:
+            # A configuration that overfills HBM does not fail cleanly here: the caching
+            # allocator's release-and-retry path calls cudaFree, a device-wide synchronisation,
+            # while NCCL kernels spin on peers -- the job hangs (seen with P2 x D2 B16 U16).
+            static, act = memory_estimate(spec, model, cfg, placement, sched, self.p)
+            total = torch.cuda.get_device_properties(self.dev).total_memory
+            if static + act + 10e9 > total:
+                raise MemoryError(
+                    f"rank {rank}: estimated peak {static / 1e9:.1f} GB static + {act / 1e9:.1f} GB activations "
+                    f"(+10 GB margin) exceeds {total / 1e9:.1f} GB; lower U or microbatch_samples, or raise P / D")
         lib.load()
         lib.call("zpp_preload_kernels")  # no lazy kernel loading once NCCL kernels can spin
         self.tasks = list(sched.per_device[self.p])

@@ -271,3 +271,27 @@ def nccl_bytes_per_step(spec: GPTSpec, cfg, placement, sched, p: int) -> tuple[i
         elif t.kind in (TaskKind.RS_GRAD_INTER, TaskKind.AG_PARAM_INTER) and n > 1:
             inter += sum((n - 1) * (lay.shard_numel // sub) * 2 for lay in lays.values())
     return intra, inter
+
+
+def memory_estimate(spec: GPTSpec, model, cfg, placement, sched, p: int) -> tuple[float, float]:
+    """(static, activation) bytes pipeline rank ``p`` will hold at peak.
+
+    static: per local stage the gathered bf16 stage (2 B/param), the fp32 master / exp_avg /
+    exp_avg_sq / shard grad (16 B per shard param) and, at D > 1, the fp32 full-stage grad.
+    activations: the reference simulator's live-micro-batch peak (`simulation.py:219-280`)
+    with the engine's real per-layer stash (planner.engine_memory_model).  Measured peaks are
+    1-9 GB above this (GEMM workspaces, logits, NCCL buffers; profiles/r02)."""
+    import dataclasses
+    from ..config import CommCostModel
+    from ..planner import engine_memory_model
+    from ..simulation import simulate
+    D = cfg.dp_size
+    static = 0
+    for s in placement.device_stages(p):
+        n = stage_layout(spec, s, cfg.num_stages, placement.stage_to_layers[s], D, optimizer_sub(cfg)).numel
+        static += 2 * n + 16 * n // D + (4 * n if D > 1 else 0)
+    fitted, _ = engine_memory_model(spec, model)
+    fitted = dataclasses.replace(fitted, weight_mem_per_layer=1e-9)  # activations only
+    sim = simulate(sched, fitted, dataclasses.replace(cfg, optimizer_state_multiplier=0.0), placement,
+                   CommCostModel(intra_node_bandwidth=1e12, inter_node_bandwidth=1e12))
+    return float(static), float(sim.peak_mem[p])

@@ -75,3 +75,26 @@ def test_opt_chunks_partition_stage(spec, P, V):
         for sl in lay.slots:
             key = "embed" if sl.name in ("wte", "wpe") else "head" if sl.layer is None else sl.layer
             assert ch[key][0] <= sl.offset and sl.offset + sl.numel <= ch[key][1]
+
+
+def test_memory_estimate_matches_measured_peaks():
+    """memory_estimate (the Runtime's refuse-to-hang guard) against the measured max_mem_gb of
+    the r02 bench lines: within 0-10 GB below; P2 x D2 B16 U16 (which hung on a 4-GPU box when
+    it overfilled HBM) is refused at 180 GB."""
+    from paper_2402_03791_b200 import ModelSpec, ParallelConfig, generate, make_placement
+    from paper_2402_03791_b200.engine.model import memory_estimate
+
+    def est(spec, P, D, B, U, V):
+        model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
+        cfg = ParallelConfig(pp_size=P, dp_size=D, microbatches=B, unit_size=U, stages_per_device=V,
+                             microbatch_samples=spec.microbatch_samples)
+        pl = make_placement(cfg, model)
+        sched = generate(model, cfg, pl)
+        return max(sum(memory_estimate(spec, model, cfg, pl, sched, p)) for p in range(P)) / 1e9
+
+    g = GPTSpec.gpt_6p2b(microbatch_samples=2)
+    for (P, D, B, U, V), measured in (((1, 1, 8, 2, 1), 159.3), ((2, 1, 16, 8, 2), 134.5), ((2, 2, 16, 8, 2), 126.3)):
+        e = est(g, P, D, B, U, V)
+        assert measured - 10 <= e <= measured, (P, D, B, U, V, e)
+    assert est(GPTSpec.gpt_13b(), 4, 1, 16, 8, 1) <= 90.3
+    assert est(g, 2, 2, 16, 16, 2) + 10 > 183.0
