@@ -41,9 +41,12 @@ typedef __nv_bfloat16 bf16;
 #ifdef ZPP_TRACE
 // Debug build only (make trace): clock64 stamps of CTA 0, [kernel][slot][tile], read by tools/attn_trace.py
 __device__ unsigned long long g_attn_trace[2][8][64];
+#ifndef ZPP_TRACE_CTA
+#define ZPP_TRACE_CTA 0  // which CTA is traced (e.g. -DZPP_TRACE_CTA=640: a CTA of the 5th wave)
+#endif
 #define ZTRACE(k, slot, t) \
   do {                     \
-    if (blockIdx.x == 0 && (t) < 64) g_attn_trace[k][slot][t] = clock64(); \
+    if (blockIdx.x == ZPP_TRACE_CTA && (t) < 64) g_attn_trace[k][slot][t] = clock64(); \
   } while (0)
 #else
 #define ZTRACE(k, slot, t) \
@@ -74,42 +77,31 @@ __device__ __forceinline__ void warp_arrive(uint32_t bar) {
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 
-// Thread = TMEM lane r of a 128-row accumulator, half hh of its D columns -> bf16 row segment.
-template <int D>
-__device__ __forceinline__ void store_acc_row(uint32_t tacc, uint32_t lo, int hh, bf16* dst) {
-#pragma unroll 1
-  for (int c = hh * (D / 64); c < (hh + 1) * (D / 64); ++c) {
-    uint32_t v[32];
-    tmem_ld32(tacc + lo + c * 32, v);
-    tmem_wait_ld();
-#pragma unroll
-    for (int k = 0; k < 32; k += 8)
-      *reinterpret_cast<uint4*>(dst + c * 32 + k) =
-          make_uint4(pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
-                     pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
-                     pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
-                     pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
-  }
-}
-// Thread = TMEM lane r of a 128-row accumulator, quarter `part` of its D columns -> bf16.
-template <int D>
-__device__ __forceinline__ void store_acc_quarter(uint32_t tacc, uint32_t lo, int part, bf16* dst) {
-  constexpr int W = D / 4;  // 32 or 16 columns
+// Epilogue staging: thread = TMEM lane r of a 128-row fp32 accumulator, columns [c0, c0 + W)
+// -> bf16 into a 128B-swizzled smem tile of [128 rows][64 cols] atoms (the TMA box layout), so
+// one thread can then TMA-store the whole tile: each warp writing 32 different rows straight
+// to global memory cost ~4k cycles of uncoalesced stores per tile (measured, dK/dV epilogue).
+template <int W>
+__device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int c0, uint32_t tile) {
   uint32_t v[32];
   if constexpr (W == 32) {
-    tmem_ld32(tacc + lo + part * 32, v);
+    tmem_ld32(tacc + lo + c0, v);
   } else {
-    tmem_ld16(tacc + lo + part * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
+    tmem_ld16(tacc + lo + c0, *reinterpret_cast<uint32_t(*)[16]>(v));
   }
   tmem_wait_ld();
 #pragma unroll
-  for (int k = 0; k < W; k += 8)
-    *reinterpret_cast<uint4*>(dst + part * W + k) =
-        make_uint4(pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
-                   pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
-                   pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
-                   pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
+  for (int k = 0; k < W; k += 8) {
+    const int col = c0 + k;  // multiple of 8: one 16-byte chunk
+    const uint32_t atom = tile + (col >> 6) * (128 * 128), chunk = (col & 63) >> 3;
+    st_shared_v4(atom + r * 128 + ((chunk ^ (r & 7)) << 4),
+                 pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                 pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
+                 pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
+                 pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
+  }
 }
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
@@ -139,7 +131,8 @@ struct BwdDqCfg {
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
-                       const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ out,
+                       const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_st,
+                       const bf16* __restrict__ out,
                        const float* __restrict__ lse, float* __restrict__ delta_out, float* __restrict__ lse2_out,
                        bf16* __restrict__ dqkv, int T, int H, int BH, float scale) {
   using C = BwdDqCfg<D>;
@@ -388,7 +381,15 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(dq_done, 0);
     if (threadIdx.x == 128) ZTRACE(0, 4, 63);
     tc_fence_after();
-    store_acc_row<D>(T_DQ, lo, hh, dqkv + ((long long)row_base + q0 + r) * 3 * H * D + (long long)h * D);
+    // dQ -> swizzled smem (the Q tile's slot: Q lives in TMEM now) -> TMA store
+    for (int c = hh * (D / 2); c < (hh + 1) * (D / 2); c += 32) stage_acc<32>(T_DQ, lo, r, c, base + C::Q_OFF);
+    fence_proxy_async();
+    named_bar_sync(1, 256);
+    if (threadIdx.x == 128) {
+      for (int a = 0; a < NA; ++a) tma_store_2d(&tm_st, base + C::Q_OFF + a * C::QATOM, h * D + 64 * a, row_base + q0);
+      bulk_commit();
+      bulk_wait_all();
+    }
     if (threadIdx.x == 128) ZTRACE(0, 5, 63);
   }
   tc_fence_before();
@@ -425,12 +426,14 @@ struct BwdDkdvCfg {
   static constexpr int BAR_OFF = L_OFF + QST * 512;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "smem budget");
+  static_assert(2 * KTILE <= 2 * QST * QTILE, "dK / dV staging reuses the Q / dO ring");
 };
 
 template <int D>
 __global__ void __launch_bounds__(640, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
-                         const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse2,
+                         const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_st,
+                         const float* __restrict__ lse2,
                          const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, int BH,
                          float scale) {
   using C = BwdDkdvCfg<D>;
@@ -645,9 +648,20 @@ __global__ void __launch_bounds__(640, 1)
     mbar_wait(mm_done, 0);
     if (threadIdx.x == 128) ZTRACE(1, 4, 63);
     tc_fence_after();
-    bf16* dk = dqkv + ((long long)row_base + k0 + r) * 3 * H * D + (long long)H * D + (long long)h * D;
-    store_acc_quarter<D>(T_DK, lo, part, dk);
-    store_acc_quarter<D>(T_DV, lo, part, dk + (long long)H * D);
+    // dK, dV -> swizzled smem tiles (the drained Q/dO ring) -> TMA stores
+    const uint32_t st_k = base + C::Q_OFF, st_v = st_k + C::KTILE;
+    stage_acc<D / 4>(T_DK, lo, r, part * (D / 4), st_k);
+    stage_acc<D / 4>(T_DV, lo, r, part * (D / 4), st_v);
+    fence_proxy_async();
+    named_bar_sync(1, 512);
+    if (threadIdx.x == 128) {
+      for (int a = 0; a < NA; ++a) {
+        tma_store_2d(&tm_st, st_k + a * C::KATOM, H * D + h * D + 64 * a, row_base + k0);
+        tma_store_2d(&tm_st, st_v + a * C::KATOM, 2 * H * D + h * D + 64 * a, row_base + k0);
+      }
+      bulk_commit();
+      bulk_wait_all();
+    }
     if (threadIdx.x == 128) ZTRACE(1, 5, 63);
   }
   tc_fence_before();
@@ -682,13 +696,14 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
                        int B, int T, int H, cudaStream_t s) {
   if (T % 128) return set_error(ZPP_ERR_ARG, "attn_bwd: seq must be a multiple of 128");
   const int BT = B * T;
-  CUtensorMap m_q128, m_kv64, m_kv128, m_q64, m_do128, m_do64;
+  CUtensorMap m_q128, m_kv64, m_kv128, m_q64, m_do128, m_do64, m_st;
   int rc = qkv_map(&m_q128, qkv, H, D, 3, BT, 128);
   if (!rc) rc = qkv_map(&m_kv64, qkv, H, D, 3, BT, 64);
   if (!rc) rc = qkv_map(&m_kv128, qkv, H, D, 3, BT, 128);
   if (!rc) rc = qkv_map(&m_q64, qkv, H, D, 3, BT, 64);
   if (!rc) rc = qkv_map(&m_do128, dout, H, D, 1, BT, 128);
   if (!rc) rc = qkv_map(&m_do64, dout, H, D, 1, BT, 64);
+  if (!rc) rc = qkv_map(&m_st, dqkv, H, D, 3, BT, 128);  // dQ / dK / dV tile stores
   if (rc) return rc;
   static bool set = false;
   if (!set) {
@@ -701,7 +716,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
   float* lse2 = ws + (long long)BH * T;
   const float scale = 1.f / sqrtf((float)D);
   const dim3 grid((T / 128) * BH);
-  attn_bwd_dq_kernel<D><<<grid, 384, BwdDqCfg<D>::SMEM, s>>>(m_q128, m_kv64, m_do128, (const bf16*)out, lse, delta, lse2,
+  attn_bwd_dq_kernel<D><<<grid, 384, BwdDqCfg<D>::SMEM, s>>>(m_q128, m_kv64, m_do128, m_st, (const bf16*)out, lse, delta, lse2,
                                                                (bf16*)dqkv, T, H, BH, scale);
   rc = check_launch("attn_bwd_dq");
   if (rc) return rc;
@@ -717,7 +732,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, (const float*)lse2,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, m_st, (const float*)lse2,
                                      (const float*)delta, (bf16*)dqkv, T, H, BH, scale);
   if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv launch");
   return check_launch("attn_bwd_dkdv");
