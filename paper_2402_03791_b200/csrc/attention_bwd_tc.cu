@@ -68,6 +68,11 @@ __device__ __forceinline__ float dot8(uint4 a, uint4 b) {
   return fmaf(bf16hi(a.w), bf16hi(b.w), s);
 }
 
+// Persistent-kernel item order: items are sorted heaviest first; CTA c takes item
+// k*G + c in even rounds and k*G + (G-1-c) in odd rounds (boustrophedon), which balances the
+// per-CTA sums to ~98% of ideal where plain round-robin (k*G + c) reached 88%.
+__device__ __forceinline__ int snake_item(int k, int G, int c) { return k * G + ((k & 1) ? G - 1 - c : c); }
+
 // One arrival per warp on an mbarrier initialised with the number of arriving warps: a
 // 256/512-thread barrier takes every lane's arrive as a serialised shared-memory atomic, which
 // cost ~200 cycles of tensor-core idle per tile (measured).  Each lane's own prior TMEM
@@ -105,36 +110,40 @@ __device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
-// dQ (+ delta, lse2).  warp 0: TMA Q, dO once, K_j ring of 5 (K_j is read by S_j and dQ_j);
-// warp 3: TMA V_j ring of 4; warp 1: MMA issuer; warp 2: TMEM owner; warps 4..11: thread =
-// query row (TMEM lane), warp (quarter q, half hh) takes keys [32hh, 32hh+32) of each tile.
-// TMEM: S/dS [0,128) (2 x 64), dP [128,256) (2 x 64), dQ [256, 256+D).
+// dQ (+ delta, lse2), persistent: one CTA per SM walks the (128-query block, head) items
+// heaviest first (item = blockIdx.x + k * gridDim.x); the next item's Q / dO are prefetched as
+// soon as the current ones sit in TMEM, and the dQ epilogue runs on its own warps beside the
+// next item's tiles.  warp 0: TMA Q, dO per item + K_j ring of 4 (K_j feeds S_j and dQ_j);
+// warp 3: V_j ring of 3; warp 1: MMA issuer; warp 2: TMEM owner; warps 4..11: row warps,
+// thread = query row (TMEM lane), warp (quarter q, half hh) takes keys [32hh, 32hh+32) of each
+// 64-key tile; warps 12..15: epilogue (dQ TMEM -> swizzled smem -> TMA store).
+// TMEM: S/dS [0,128) (2 x 64), dP [128,256) (2 x 64), dQ [256,256+D), Q, dO (A operands of S
+// and dP as TS-mode MMAs: an SS MMA with N = 64 is bound by re-reading its 128-row A from smem).
 template <int D>
 struct BwdDqCfg {
   static constexpr int QATOM = 128 * 128;  // [128 rows][64 bf16]
   static constexpr int QTILE = (D / 64) * QATOM;
   static constexpr int KATOM = 64 * 128;   // [64 rows][64 bf16]
   static constexpr int KTILE = (D / 64) * KATOM;
-  // deep K / V rings: the load of K_{j+KST} can only start when dQ(j) retires, and at the
-  // tensor core's rate one 64-key tile takes ~0.5 us -- an L2 TMA round trip is about as long
-  static constexpr int KST = 5, VST = 4;
+  static constexpr int KST = 5, VST = 3;
   static constexpr int Q_OFF = 0;
   static constexpr int DO_OFF = Q_OFF + QTILE;
   static constexpr int K_OFF = DO_OFF + QTILE;
   static constexpr int V_OFF = K_OFF + KST * KTILE;
-  static constexpr int RED_OFF = V_OFF + VST * KTILE;  // float [2][128] delta halves
+  static constexpr int STG_OFF = V_OFF + VST * KTILE;  // dQ epilogue staging: one [128][64] atom
+  static constexpr int RED_OFF = STG_OFF + QATOM;      // float [2][128] delta halves
   static constexpr int BAR_OFF = RED_OFF + 1024;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int THREADS = 512;
   static_assert(SMEM <= 232448, "smem budget");
 };
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(512, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                        const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_st,
-                       const bf16* __restrict__ out,
-                       const float* __restrict__ lse, float* __restrict__ delta_out, float* __restrict__ lse2_out,
-                       bf16* __restrict__ dqkv, int T, int H, int BH, float scale) {
+                       const bf16* __restrict__ out, const float* __restrict__ lse, float* __restrict__ delta_out,
+                       float* __restrict__ lse2_out, int T, int H, int BH, float scale) {
   using C = BwdDqCfg<D>;
   constexpr int NA = D / 64;
   extern __shared__ uint8_t smem_raw[];
@@ -146,8 +155,8 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t qd_full = bars, k_full0 = bars + 8, k_empty0 = k_full0 + 8 * C::KST;
   const uint32_t v_full0 = k_empty0 + 8 * C::KST, v_empty0 = v_full0 + 8 * C::VST;
   const uint32_t s_full0 = v_empty0 + 8 * C::VST, dp_full0 = s_full0 + 16, ds_full0 = dp_full0 + 16;
-  const uint32_t dq_done = ds_full0 + 16, qt_full = dq_done + 8;
-  static_assert(8 * (1 + 2 * C::KST + 2 * C::VST + 8) <= 240, "barrier area");
+  const uint32_t dq_done = ds_full0 + 16, qt_full = dq_done + 8, qd_empty = qt_full + 8, dq_free = qd_empty + 8;
+  static_assert(8 * (1 + 2 * C::KST + 2 * C::VST + 10) <= 240, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -155,18 +164,20 @@ __global__ void __launch_bounds__(384, 1)
   // programmatic dependent launch: once every dQ CTA is resident, dK/dV CTAs may take the SMs
   // the dQ tail frees (they wait for our delta / lse2 with griddepcontrol.wait)
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // 1-D grid, heaviest query blocks first across ALL heads
   const int nqb = T / 128;
-  const int bh = blockIdx.x % BH, b = bh / H, h = bh % H;
-  const int qblk = nqb - 1 - static_cast<int>(blockIdx.x) / BH;
-  const int q0 = qblk * 128;
-  const int nkt = 2 * (qblk + 1);  // 64-key tiles up to the diagonal
-  const int row_base = b * T;
+  const int nitems = nqb * BH;
+  auto decode = [&](int w, int& bh, int& q0, int& nkt) {  // heaviest query blocks first, all heads
+    bh = w % BH;
+    const int qblk = nqb - 1 - w / BH;
+    q0 = qblk * 128;
+    nkt = 2 * (qblk + 1);  // 64-key tiles up to the diagonal
+  };
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_kv);
     tma_prefetch(&tm_do);
+    tma_prefetch(&tm_st);
     mbar_init(qd_full, 1);
     for (int s = 0; s < C::KST; ++s) {
       mbar_init(k_full0 + 8 * s, 1);
@@ -183,6 +194,8 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_init(dq_done, 1);
     mbar_init(qt_full, 8);
+    mbar_init(qd_empty, 8);
+    mbar_init(dq_free, 4);  // one arrival per epilogue warp
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -190,39 +203,56 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // Q and dO live in TMEM as the A operands of S and dP (TS-mode MMAs: an SS MMA with N = 64
-  // is bound by the smem read of its 128-row A operand, 48 instead of 32 cycles per K16)
   const uint32_t T_S = tmem, T_DP = tmem + 128, T_DQ = tmem + 256, T_Q = T_DQ + D, T_DO = T_Q + D / 2;
   if (threadIdx.x == 128) ZTRACE(0, 1, 63);
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(qd_full, 2 * C::QTILE);
-      for (int a = 0; a < NA; ++a) {
-        tma_load_2d(base + C::Q_OFF + a * C::QATOM, &tm_q, qd_full, h * D + 64 * a, row_base + q0);
-        tma_load_2d(base + C::DO_OFF + a * C::QATOM, &tm_do, qd_full, h * D + 64 * a, row_base + q0);
-      }
-      for (int j = 0; j < nkt; ++j) {
-        const int st = j % C::KST;
-        mbar_wait(k_empty0 + 8 * st, ((j / C::KST) & 1) ^ 1);
-        const uint32_t fb = k_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, C::KTILE);
-        for (int a = 0; a < NA; ++a)
-          tma_load_2d(base + C::K_OFF + st * C::KTILE + a * C::KATOM, &tm_kv, fb, H * D + h * D + 64 * a,
-                      row_base + j * 64);
+      int g = 0;
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, q0, nkt;
+        decode(w, bh, q0, nkt);
+        const int h = bh % H, row_base = (bh / H) * T;
+        if (j >= 1) mbar_wait(qd_empty, (j - 1) & 1);  // Q / dO of item j-1 are in TMEM
+        mbar_arrive_expect_tx(qd_full, 2 * C::QTILE);
+        for (int a = 0; a < NA; ++a) {
+          tma_load_2d(base + C::Q_OFF + a * C::QATOM, &tm_q, qd_full, h * D + 64 * a, row_base + q0);
+          tma_load_2d(base + C::DO_OFF + a * C::QATOM, &tm_do, qd_full, h * D + 64 * a, row_base + q0);
+        }
+        for (int jt = 0; jt < nkt; ++jt, ++g) {
+          const int st = g % C::KST;
+          mbar_wait(k_empty0 + 8 * st, ((g / C::KST) & 1) ^ 1);
+          const uint32_t fb = k_full0 + 8 * st;
+          mbar_arrive_expect_tx(fb, C::KTILE);
+          for (int a = 0; a < NA; ++a)
+            tma_load_2d(base + C::K_OFF + st * C::KTILE + a * C::KATOM, &tm_kv, fb, H * D + h * D + 64 * a,
+                        row_base + jt * 64);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 3) {
     if (lane == 0) {
-      for (int j = 0; j < nkt; ++j) {
-        const int st = j % C::VST;
-        mbar_wait(v_empty0 + 8 * st, ((j / C::VST) & 1) ^ 1);
-        const uint32_t fb = v_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, C::KTILE);
-        for (int a = 0; a < NA; ++a)
-          tma_load_2d(base + C::V_OFF + st * C::KTILE + a * C::KATOM, &tm_kv, fb, 2 * H * D + h * D + 64 * a,
-                      row_base + j * 64);
+      int g = 0;
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, q0, nkt;
+        decode(w, bh, q0, nkt);
+        const int h = bh % H, row_base = (bh / H) * T;
+        for (int jt = 0; jt < nkt; ++jt, ++g) {
+          const int st = g % C::VST;
+          mbar_wait(v_empty0 + 8 * st, ((g / C::VST) & 1) ^ 1);
+          const uint32_t fb = v_full0 + 8 * st;
+          mbar_arrive_expect_tx(fb, C::KTILE);
+          for (int a = 0; a < NA; ++a)
+            tma_load_2d(base + C::V_OFF + st * C::KTILE + a * C::KATOM, &tm_kv, fb, 2 * H * D + h * D + 64 * a,
+                        row_base + jt * 64);
+        }
       }
     }
     __syncwarp();
@@ -230,167 +260,213 @@ __global__ void __launch_bounds__(384, 1)
     {  // whole warp: uniform descriptors, elect.sync issues
       constexpr uint32_t id_s = make_idesc_bf16(128, 64, false, false);  // S, dP: N = 64 keys
       constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);    // dQ: B = K_j N-major (N = d)
-      auto issue_s = [&](int j) {
-        const int st = j % C::KST;
-        mbar_wait(k_full0 + 8 * st, (j / C::KST) & 1);
+      auto issue_s = [&](int g) {
+        const int st = g % C::KST;
+        mbar_wait(k_full0 + 8 * st, (g / C::KST) & 1);
         tc_fence_after();
         const uint32_t kb = base + C::K_OFF + st * C::KTILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_ts_w(T_S + (j & 1) * 64, T_Q + kk * 8,
+          mma_bf16_ts_w(T_S + (g & 1) * 64, T_Q + kk * 8,
                         make_sdesc(kb + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-        mma_commit_w(s_full0 + 8 * (j & 1));
+        mma_commit_w(s_full0 + 8 * (g & 1));
       };
-      auto issue_dp = [&](int j) {
-        const int st = j % C::VST;
-        mbar_wait(v_full0 + 8 * st, (j / C::VST) & 1);
+      auto issue_dp = [&](int g) {
+        const int st = g % C::VST;
+        mbar_wait(v_full0 + 8 * st, (g / C::VST) & 1);
         tc_fence_after();
         const uint32_t vb = base + C::V_OFF + st * C::KTILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_ts_w(T_DP + (j & 1) * 64, T_DO + kk * 8,
+          mma_bf16_ts_w(T_DP + (g & 1) * 64, T_DO + kk * 8,
                         make_sdesc(vb + (kk >> 2) * C::KATOM + (kk & 3) * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-        mma_commit_w(dp_full0 + 8 * (j & 1));
+        mma_commit_w(dp_full0 + 8 * (g & 1));
         mma_commit_w(v_empty0 + 8 * st);
       };
-      mbar_wait(qt_full, 0);  // Q, dO copied into TMEM by the row threads
-      tc_fence_after();
-      issue_s(0);
-      issue_dp(0);
-      if (nkt > 1) {
-        issue_s(1);
-        issue_dp(1);
-      }
-      for (int j = 0; j < nkt; ++j) {
-        ZTRACE(0, 0, j);
-        mbar_wait(ds_full0 + 8 * (j & 1), (j >> 1) & 1);
-        ZTRACE(0, 1, j);
+      int g = 0;
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, q0, nkt;
+        decode(w, bh, q0, nkt);
+        mbar_wait(qt_full, j & 1);  // Q, dO of item j copied into TMEM by the row warps
         tc_fence_after();
-        const uint32_t kb = base + C::K_OFF + (j % C::KST) * C::KTILE;
-        // dQ += dS K_j: A = dS in TMEM (each 32-key half packed into its first 16 columns)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_bf16_ts_w(T_DQ, T_S + (j & 1) * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
-                      make_sdesc(kb + kk * 2048, C::KATOM, 1024), id_q, (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(k_empty0 + 8 * (j % C::KST));
-        if (j + 2 < nkt) {  // buffers (j & 1): dS_j read by the dQ MMA above (in-order pipe)
-          issue_s(j + 2);
-          ZTRACE(0, 2, j);
-          issue_dp(j + 2);
+        issue_s(g);
+        issue_dp(g);
+        if (nkt > 1) {
+          issue_s(g + 1);
+          issue_dp(g + 1);
         }
-        ZTRACE(0, 3, j);
+        for (int jt = 0; jt < nkt; ++jt, ++g) {
+          if (j < 8) ZTRACE(0, 0, jt);
+          mbar_wait(ds_full0 + 8 * (g & 1), (g >> 1) & 1);
+          if (j < 8) ZTRACE(0, 1, jt);
+          tc_fence_after();
+          if (jt == 0 && j > 0) {
+            mbar_wait(dq_free, (j - 1) & 1);  // the epilogue warps have read dQ of item j-1
+            tc_fence_after();
+          }
+          const uint32_t kb = base + C::K_OFF + (g % C::KST) * C::KTILE;
+          // dQ += dS K_j: A = dS in TMEM (each 32-key half packed into its first 16 columns)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16_ts_w(T_DQ, T_S + (g & 1) * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                          make_sdesc(kb + kk * 2048, C::KATOM, 1024), id_q, (jt > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_w(k_empty0 + 8 * (g % C::KST));
+          if (jt + 2 < nkt) {  // buffers (g & 1): dS_g read by the dQ MMA above (in-order pipe)
+            issue_s(g + 2);
+            if (j < 8) ZTRACE(0, 2, jt);
+            issue_dp(g + 2);
+          }
+          if (j < 8) ZTRACE(0, 3, jt);
+        }
+        mma_commit_w(dq_done);
       }
-      mma_commit_w(dq_done);
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 12) {
     const int q = warp & 3;
     const int hh = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // query row == TMEM lane
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * kLog2e;
-    const float lse2_r = lse[(long long)bh * T + q0 + r] * kLog2e;
-    // delta = rowsum(O * dO): this thread sums half hh of the row's D columns (O from global,
-    // read once here; dO from the swizzled smem tile)
     constexpr int CH = D / 16;  // 16-byte chunks per half row
-    uint4 ov[CH];
-    const uint4* orow = reinterpret_cast<const uint4*>(out + ((long long)row_base + q0 + r) * H * D + h * D) + hh * CH;
+    int g = 0;
+    for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+      int bh, q0, nkt;
+      decode(w, bh, q0, nkt);
+      const int h = bh % H, row_base = (bh / H) * T;
+      const float lse2_r = lse[(long long)bh * T + q0 + r] * kLog2e;
+      // delta = rowsum(O * dO): this thread sums half hh of the row's D columns (O from global,
+      // read once here; dO from the swizzled smem tile)
+      uint4 ov[CH];
+      const uint4* orow =
+          reinterpret_cast<const uint4*>(out + ((long long)row_base + q0 + r) * H * D + h * D) + hh * CH;
 #pragma unroll
-    for (int i = 0; i < CH; ++i) ov[i] = __ldg(orow + i);
-    mbar_wait(qd_full, 0);
-    if (threadIdx.x == 128) ZTRACE(0, 2, 63);
-    float acc = 0.f;
-    {
-      // this thread's half row of Q and dO -> TMEM (lane r, packed bf16 pairs), and delta
-      uint32_t qv[4 * CH], dv[4 * CH];
-#pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        const int cg = hh * CH + i;  // global chunk index along D
-        const uint32_t off = (cg >> 3) * C::QATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
-        const uint4 d4 = ld_shared_v4(base + C::DO_OFF + off);
-        const uint4 q4 = ld_shared_v4(base + C::Q_OFF + off);
-        acc += dot8(ov[i], d4);
-        dv[4 * i] = d4.x, dv[4 * i + 1] = d4.y, dv[4 * i + 2] = d4.z, dv[4 * i + 3] = d4.w;
-        qv[4 * i] = q4.x, qv[4 * i + 1] = q4.y, qv[4 * i + 2] = q4.z, qv[4 * i + 3] = q4.w;
-      }
-      if constexpr (CH == 8) {
-        tmem_st32(T_Q + lo + hh * 32, qv);
-        tmem_st32(T_DO + lo + hh * 32, dv);
-      } else {
-        tmem_st16(T_Q + lo + hh * 16, qv);
-        tmem_st16(T_DO + lo + hh * 16, dv);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      warp_arrive(qt_full);
-    }
-    red[hh * 128 + r] = acc;
-    named_bar_sync(1, 256);
-    const float delta_r = red[r] + red[128 + r];
-    if (hh == 0) {
-      delta_out[(long long)bh * T + q0 + r] = delta_r;
-      lse2_out[(long long)bh * T + q0 + r] = lse2_r;
-    }
-    for (int j = 0; j < nkt; ++j) {
-      const int buf = j & 1;
-      const uint32_t par = (j >> 1) & 1;
-      const uint32_t ts = T_S + lo + buf * 64 + hh * 32;
-#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (softmax warps only hand over)
-      mbar_wait(s_full0 + 8 * buf, par);
-      mbar_wait(dp_full0 + 8 * buf, par);
-      tc_fence_before();
-      warp_arrive(ds_full0 + 8 * buf);
-      if (threadIdx.x == 128) ZTRACE(0, 7, j);
-      continue;
-#endif
-      if (threadIdx.x == 128) ZTRACE(0, 4, j);
-      mbar_wait(s_full0 + 8 * buf, par);
-      if (threadIdx.x == 128) ZTRACE(0, 5, j);
-      tc_fence_after();
-      float p[32];
+      for (int i = 0; i < CH; ++i) ov[i] = __ldg(orow + i);
+      mbar_wait(qd_full, j & 1);
+      if (threadIdx.x == 128 && j == 0) ZTRACE(0, 2, 63);
+      float acc = 0.f;
       {
+        // this thread's half row of Q and dO -> TMEM (lane r, packed bf16 pairs), and delta.
+        // TMEM Q / dO are free: the S / dP MMAs of item j-1 completed before its last tile's
+        // s_full / dp_full, which this warp has consumed.
+        uint32_t qv[4 * CH], dv[4 * CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const int cg = hh * CH + i;  // global chunk index along D
+          const uint32_t off = (cg >> 3) * C::QATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
+          const uint4 d4 = ld_shared_v4(base + C::DO_OFF + off);
+          const uint4 q4 = ld_shared_v4(base + C::Q_OFF + off);
+          acc += dot8(ov[i], d4);
+          dv[4 * i] = d4.x, dv[4 * i + 1] = d4.y, dv[4 * i + 2] = d4.z, dv[4 * i + 3] = d4.w;
+          qv[4 * i] = q4.x, qv[4 * i + 1] = q4.y, qv[4 * i + 2] = q4.z, qv[4 * i + 3] = q4.w;
+        }
+        if constexpr (CH == 8) {
+          tmem_st32(T_Q + lo + hh * 32, qv);
+          tmem_st32(T_DO + lo + hh * 32, dv);
+        } else {
+          tmem_st16(T_Q + lo + hh * 16, qv);
+          tmem_st16(T_DO + lo + hh * 16, dv);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(qt_full);
+        warp_arrive(qd_empty);  // Q / dO smem may take the next item's tiles
+      }
+      red[hh * 128 + r] = acc;
+      named_bar_sync(1, 256);
+      const float delta_r = red[r] + red[128 + r];
+      named_bar_sync(1, 256);  // red is rewritten by the next item
+      if (hh == 0) {
+        delta_out[(long long)bh * T + q0 + r] = delta_r;
+        lse2_out[(long long)bh * T + q0 + r] = lse2_r;
+      }
+      for (int jt = 0; jt < nkt; ++jt, ++g) {
+        const int buf = g & 1;
+        const uint32_t par = (g >> 1) & 1;
+        const uint32_t ts = T_S + lo + buf * 64 + hh * 32;
+#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (row warps only hand over)
+        mbar_wait(s_full0 + 8 * buf, par);
+        mbar_wait(dp_full0 + 8 * buf, par);
+        tc_fence_before();
+        warp_arrive(ds_full0 + 8 * buf);
+        continue;
+#endif
+        if (threadIdx.x == 128 && j < 8) ZTRACE(0, 4, jt);
+        mbar_wait(s_full0 + 8 * buf, par);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(0, 5, jt);
+        tc_fence_after();
+        float p[32];
+        {
+          uint32_t v[32];
+          tmem_ld32(ts, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) p[k] = fast_exp2(fmaf(__uint_as_float(v[k]), sl2, -lse2_r));
+        }
+        if (jt >= nkt - 2) {  // the two tiles that straddle the diagonal: keys after the query
+          const int kq = jt * 64 + hh * 32 - q0 - r;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (kq + k > 0) p[k] = 0.f;
+        }
+        if (threadIdx.x == 128 && j < 8) ZTRACE(0, 6, jt);
+        mbar_wait(dp_full0 + 8 * buf, par);
+        tc_fence_after();
         uint32_t v[32];
-        tmem_ld32(ts, v);
+        tmem_ld32(T_DP + lo + buf * 64 + hh * 32, v);
         tmem_wait_ld();
+        uint32_t pk[16];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) p[k] = fast_exp2(fmaf(__uint_as_float(v[k]), sl2, -lse2_r));
+        for (int k = 0; k < 16; ++k)
+          pk[k] = pack_bf16(p[2 * k] * (__uint_as_float(v[2 * k]) - delta_r) * scale,
+                            p[2 * k + 1] * (__uint_as_float(v[2 * k + 1]) - delta_r) * scale);
+        tmem_st16(ts, pk);  // over S columns this warp has already read
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(ds_full0 + 8 * buf);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(0, 7, jt);
       }
-      if (j >= nkt - 2) {  // the two tiles that straddle the diagonal: keys after the query
-        const int kq = j * 64 + hh * 32 - q0 - r;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (kq + k > 0) p[k] = 0.f;
-      }
-      if (threadIdx.x == 128) ZTRACE(0, 6, j);
-      mbar_wait(dp_full0 + 8 * buf, par);
+    }
+  } else if (warp >= 12) {
+    // epilogue warps: thread = TMEM lane (query row) r of quarter q, all D columns
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
+    for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+      int bh, q0, nkt;
+      decode(w, bh, q0, nkt);
+      const int h = bh % H, row_base = (bh / H) * T;
+      mbar_wait(dq_done, j & 1);
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(T_DP + lo + buf * 64 + hh * 32, v);
-      tmem_wait_ld();
-      uint32_t pk[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        pk[k] = pack_bf16(p[2 * k] * (__uint_as_float(v[2 * k]) - delta_r) * scale,
-                          p[2 * k + 1] * (__uint_as_float(v[2 * k + 1]) - delta_r) * scale);
-      tmem_st16(ts, pk);  // over S columns this warp has already read
-      tmem_wait_st();
-      tc_fence_before();
-      warp_arrive(ds_full0 + 8 * buf);
-      if (threadIdx.x == 128) ZTRACE(0, 7, j);
+#pragma unroll 1
+      for (int a = 0; a < NA; ++a) {  // one 64-column atom at a time through a 16 KB staging tile
+        named_bar_sync(2, 128);       // the previous TMA store has left the staging tile
+        stage_acc<32>(T_DQ, lo, r, 64 * a, base + C::STG_OFF - 64 * a * 256);
+        stage_acc<32>(T_DQ, lo, r, 64 * a + 32, base + C::STG_OFF - 64 * a * 256);
+        if (a == NA - 1) {
+          tc_fence_before();
+          warp_arrive(dq_free);  // dQ read: the next item may accumulate into it
+        }
+        fence_proxy_async();
+        named_bar_sync(2, 128);
+        if (threadIdx.x == 384) {
+          tma_store_2d(&tm_st, base + C::STG_OFF, h * D + 64 * a, row_base + q0);
+          bulk_commit();
+          bulk_wait_all();
+        }
+      }
+      if (threadIdx.x == 384 && j == 0) ZTRACE(0, 5, 63);
+      if (threadIdx.x == 384 && j == 0) ZTRACE(0, 4, 63);
     }
-    mbar_wait(dq_done, 0);
-    if (threadIdx.x == 128) ZTRACE(0, 4, 63);
-    tc_fence_after();
-    // dQ -> swizzled smem (the Q tile's slot: Q lives in TMEM now) -> TMA store
-    for (int c = hh * (D / 2); c < (hh + 1) * (D / 2); c += 32) stage_acc<32>(T_DQ, lo, r, c, base + C::Q_OFF);
-    fence_proxy_async();
-    named_bar_sync(1, 256);
-    if (threadIdx.x == 128) {
-      for (int a = 0; a < NA; ++a) tma_store_2d(&tm_st, base + C::Q_OFF + a * C::QATOM, h * D + 64 * a, row_base + q0);
-      bulk_commit();
-      bulk_wait_all();
-    }
-    if (threadIdx.x == 128) ZTRACE(0, 5, 63);
   }
   tc_fence_before();
   __syncthreads();
@@ -399,14 +475,19 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// dK / dV.  warp 0: TMA K, V once, then Q_t / dO_t (+ lse2_t, delta_t) through a ring of 3;
-// warp 1: MMA issuer; warp 2: TMEM owner; warps 4..19: thread = key row (TMEM lane), warp
-// (quarter q, part) takes queries [16 part, 16 part + 16) of each 64-query tile.
-// K and V are copied into TMEM once (the A operands of S^T / dP^T: TS-mode MMAs run at the
-// tensor core's rate for N = 64, the SS form is bound by re-reading the 128-row A from smem).
-// S^T / dP^T are single-buffered but released as soon as the row threads have loaded them,
-// so S^T(t+1), dP^T(t+1) run while the exp2 phase of tile t does; P^T and dS^T go to smem
-// (the A operands of dV += P^T dO and dK += dS^T Q, N = d = 128: full rate from smem).
+// dK / dV, persistent: one CTA per SM walks the (128-key block, head) items heaviest first
+// (item = blockIdx.x + k * gridDim.x), so the next item's K / V load, their copy into TMEM and
+// its first S^T / dP^T MMAs overlap the previous item's last tiles and its dK / dV epilogue
+// (a CTA per item paid ~6k cycles of prologue + ~3k of epilogue on ~25k of tiles).
+// warp 0: TMA (K, V per item; Q_t / dO_t + lse2_t / delta_t through a ring of 3, continuing
+// across items); warp 1: MMA issuer; warp 2: TMEM owner; warps 4..19: row warps, thread = key
+// row (TMEM lane), warp (quarter q, part) takes queries [16 part, 16 part + 16) of each
+// 64-query tile; warps 20..23: epilogue (dK / dV TMEM -> swizzled smem -> TMA store).
+// K and V live in TMEM (A operands of S^T / dP^T: TS-mode MMAs run at the tensor core's rate
+// for N = 64; the SS form re-reads the 128-row A from smem).  S^T / dP^T are single-buffered
+// but released as soon as the row warps have loaded them; P^T and dS^T go to smem (A operands
+// of dV += P^T dO and dK += dS^T Q, N = d: full rate from smem).  The K / V smem tiles double
+// as the epilogue staging area once K / V of the next item sit in TMEM.
 // TMEM: dV [0,D) dK [D,2D) K [2D,2D+D/2) V [2D+D/2,3D) S^T [3D,3D+64) dP^T [3D+64,3D+128).
 template <int D>
 struct BwdDkdvCfg {
@@ -425,16 +506,15 @@ struct BwdDkdvCfg {
   static constexpr int L_OFF = DS_OFF + PT_BYTES;  // per stage: lse2 [64] | delta [64]
   static constexpr int BAR_OFF = L_OFF + QST * 512;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int THREADS = 768;
   static_assert(SMEM <= 232448, "smem budget");
-  static_assert(2 * KTILE <= 2 * QST * QTILE, "dK / dV staging reuses the Q / dO ring");
 };
 
 template <int D>
-__global__ void __launch_bounds__(640, 1)
+__global__ void __launch_bounds__(768, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_st,
-                         const float* __restrict__ lse2,
-                         const float* __restrict__ delta, bf16* __restrict__ dqkv, int T, int H, int BH,
+                         const float* __restrict__ lse2, const float* __restrict__ delta, int T, int H, int BH,
                          float scale) {
   using C = BwdDkdvCfg<D>;
   constexpr int NA = D / 64;
@@ -446,20 +526,25 @@ __global__ void __launch_bounds__(640, 1)
   const uint32_t kv_full = bars, qd_full0 = bars + 8, qd_empty0 = qd_full0 + 8 * C::QST;
   const uint32_t kv_tmem = qd_empty0 + 8 * C::QST, sp_full = kv_tmem + 8, sp_free = sp_full + 8;
   const uint32_t ds_full = sp_free + 8, ds_free = ds_full + 8, mm_done = ds_free + 8;
+  const uint32_t acc_free = mm_done + 8, kv_empty = acc_free + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nitems = (T / 128) * BH;
   if (threadIdx.x == 128) ZTRACE(1, 0, 63);
-  const int bh = blockIdx.x % BH, b = bh / H, h = bh % H;
-  const int kblk = static_cast<int>(blockIdx.x) / BH;  // block 0 has the most query tiles: first
-  const int k0 = kblk * 128;
-  const int nq = 2 * (T / 128 - kblk);  // 64-query tiles from the diagonal on
-  const int row_base = b * T;
+  // item w -> (key block, head); item 0.. have the most query tiles
+  auto decode = [&](int w, int& bh, int& k0, int& nq) {
+    bh = w % BH;
+    const int kblk = w / BH;
+    k0 = kblk * 128;
+    nq = 2 * (T / 128 - kblk);
+  };
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tm_kv);
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
+    tma_prefetch(&tm_st);
     mbar_init(kv_full, 1);
     for (int s = 0; s < C::QST; ++s) {
       mbar_init(qd_full0 + 8 * s, 1);
@@ -471,6 +556,8 @@ __global__ void __launch_bounds__(640, 1)
     mbar_init(ds_full, 16);
     mbar_init(ds_free, 1);
     mbar_init(mm_done, 1);
+    mbar_init(acc_free, 4);  // one arrival per epilogue warp
+    mbar_init(kv_empty, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -483,24 +570,38 @@ __global__ void __launch_bounds__(640, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * C::KTILE);
-      for (int a = 0; a < NA; ++a) {
-        tma_load_2d(base + C::K_OFF + a * C::KATOM, &tm_kv, kv_full, H * D + h * D + 64 * a, row_base + k0);
-        tma_load_2d(base + C::V_OFF + a * C::KATOM, &tm_kv, kv_full, 2 * H * D + h * D + 64 * a, row_base + k0);
-      }
-      for (int it = 0; it < nq; ++it) {
-        const int st = it % C::QST;
-        const int q0 = k0 + it * 64;
-        mbar_wait(qd_empty0 + 8 * st, ((it / C::QST) & 1) ^ 1);
-        const uint32_t fb = qd_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, 2 * C::QTILE + 512);
+      int g = 0;  // running tile index of this CTA (ring stage / parity)
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, k0, nq;
+        decode(w, bh, k0, nq);
+        const int b = bh / H, h = bh % H, row_base = b * T;
+        // K / V smem is free once K / V(j-1) sit in TMEM (j == 1) and, from j == 2 on, once the
+        // epilogue of item j-2 (staged in the same smem) has been stored
+        if (j == 1) mbar_wait(kv_tmem, 0);
+        if (j >= 2) mbar_wait(kv_empty, (j - 2) & 1);
+        mbar_arrive_expect_tx(kv_full, 2 * C::KTILE);
         for (int a = 0; a < NA; ++a) {
-          tma_load_2d(base + C::Q_OFF + st * C::QTILE + a * C::QATOM, &tm_q, fb, h * D + 64 * a, row_base + q0);
-          tma_load_2d(base + C::DO_OFF + st * C::QTILE + a * C::QATOM, &tm_do, fb, h * D + 64 * a, row_base + q0);
+          tma_load_2d(base + C::K_OFF + a * C::KATOM, &tm_kv, kv_full, H * D + h * D + 64 * a, row_base + k0);
+          tma_load_2d(base + C::V_OFF + a * C::KATOM, &tm_kv, kv_full, 2 * H * D + h * D + 64 * a, row_base + k0);
         }
-        if (it == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // delta / lse2 of the dQ kernel
-        bulk_load_1d(base + C::L_OFF + st * 512, lse2 + (long long)bh * T + q0, 256, fb);
-        bulk_load_1d(base + C::L_OFF + st * 512 + 256, delta + (long long)bh * T + q0, 256, fb);
+        for (int it = 0; it < nq; ++it, ++g) {
+          const int st = g % C::QST;
+          const int q0 = k0 + it * 64;
+          mbar_wait(qd_empty0 + 8 * st, ((g / C::QST) & 1) ^ 1);
+          const uint32_t fb = qd_full0 + 8 * st;
+          mbar_arrive_expect_tx(fb, 2 * C::QTILE + 512);
+          for (int a = 0; a < NA; ++a) {
+            tma_load_2d(base + C::Q_OFF + st * C::QTILE + a * C::QATOM, &tm_q, fb, h * D + 64 * a, row_base + q0);
+            tma_load_2d(base + C::DO_OFF + st * C::QTILE + a * C::QATOM, &tm_do, fb, h * D + 64 * a,
+                        row_base + q0);
+          }
+          if (g == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // delta / lse2 of the dQ kernel
+          bulk_load_1d(base + C::L_OFF + st * 512, lse2 + (long long)bh * T + q0, 256, fb);
+          bulk_load_1d(base + C::L_OFF + st * 512 + 256, delta + (long long)bh * T + q0, 256, fb);
+        }
       }
     }
     __syncwarp();
@@ -508,9 +609,9 @@ __global__ void __launch_bounds__(640, 1)
     {  // whole warp: uniform descriptors, elect.sync issues
       constexpr uint32_t id_sp = make_idesc_bf16(128, 64, false, false);  // S^T, dP^T: N = 64 queries
       constexpr uint32_t id_kv = make_idesc_bf16(128, D, false, true);    // dV, dK: B N-major (N = d)
-      auto issue_sp = [&](int it) {  // S^T = K Q^T, dP^T = V dO^T (A = K / V from TMEM)
-        const int st = it % C::QST;
-        mbar_wait(qd_full0 + 8 * st, (it / C::QST) & 1);
+      auto issue_sp = [&](int g) {  // S^T = K Q^T, dP^T = V dO^T of running tile g (A = K / V from TMEM)
+        const int st = g % C::QST;
+        mbar_wait(qd_full0 + 8 * st, (g / C::QST) & 1);
         tc_fence_after();
         const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
 #pragma unroll
@@ -523,146 +624,183 @@ __global__ void __launch_bounds__(640, 1)
                         id_sp, kk > 0 ? 1u : 0u);
         mma_commit_w(sp_full);
       };
-      mbar_wait(kv_tmem, 0);  // K, V copied into TMEM by the row threads
-      tc_fence_after();
-      issue_sp(0);
-      for (int it = 0; it < nq; ++it) {
-        const int st = it % C::QST;
-        const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
-        if (it + 1 < nq) {
-          mbar_wait(sp_free, it & 1);  // the row threads have loaded S^T(it), dP^T(it)
-          tc_fence_after();
-          issue_sp(it + 1);
-        }
-        ZTRACE(1, 0, it);
-        mbar_wait(ds_full, it & 1);
-        ZTRACE(1, 1, it);
+      int g = 0;
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, k0, nq;
+        decode(w, bh, k0, nq);
+        mbar_wait(kv_tmem, j & 1);  // K, V(j) copied into TMEM; S^T / dP^T of item j-1 loaded
         tc_fence_after();
-        const uint32_t acc0 = it > 0 ? 1u : 0u;
+        issue_sp(g);
+        for (int it = 0; it < nq; ++it, ++g) {
+          const int st = g % C::QST;
+          const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+          if (it + 1 < nq) {
+            mbar_wait(sp_free, g & 1);  // the row warps have loaded S^T(g), dP^T(g)
+            tc_fence_after();
+            issue_sp(g + 1);
+          }
+          if (j < 8) ZTRACE(1, 0, it);
+          mbar_wait(ds_full, g & 1);
+          if (j < 8) ZTRACE(1, 1, it);
+          tc_fence_after();
+          if (it == 0 && j > 0) {
+            mbar_wait(acc_free, (j - 1) & 1);  // the epilogue has read dK / dV of item j-1
+            tc_fence_after();
+          }
+          const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO: A = P^T (smem K-major), B = dO (N-major)
-          mma_bf16_w(T_DV, make_sdesc(base + C::PT_OFF + kk * 32, 16, 1024), make_sdesc(dos + kk * 2048, C::QATOM, 1024),
-                     id_kv, (acc0 | kk) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO: A = P^T (smem K-major), B = dO (N-major)
+            mma_bf16_w(T_DV, make_sdesc(base + C::PT_OFF + kk * 32, 16, 1024),
+                       make_sdesc(dos + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q: A = dS^T (smem K-major), B = Q (N-major)
-          mma_bf16_w(T_DK, make_sdesc(base + C::DS_OFF + kk * 32, 16, 1024), make_sdesc(qs + kk * 2048, C::QATOM, 1024),
-                     id_kv, (acc0 | kk) ? 1u : 0u);
-        mma_commit_w(ds_free);
-        mma_commit_w(qd_empty0 + 8 * st);
-        ZTRACE(1, 2, it);
+          for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q: A = dS^T (smem K-major), B = Q (N-major)
+            mma_bf16_w(T_DK, make_sdesc(base + C::DS_OFF + kk * 32, 16, 1024),
+                       make_sdesc(qs + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
+          mma_commit_w(ds_free);
+          mma_commit_w(qd_empty0 + 8 * st);
+          if (j < 8) ZTRACE(1, 2, it);
+        }
+        mma_commit_w(mm_done);
       }
-      mma_commit_w(mm_done);
     }
     __syncwarp();
-  } else if (warp >= 4) {
-    // 16 row warps (4 per SM sub-partition): warp (quarter q, part) owns key rows 32q..32q+31
-    // and queries [16 part, 16 part + 16) of each tile -- enough warps in flight to hide the
-    // TMEM-load -> exp2 -> smem-store latency chain (with 8 warps the exp2 phase, not the
-    // tensor core, set the pace: ~1000 cycles per tile vs ~1024 of MMA work)
+  } else if (warp >= 4 && warp < 20) {
     const int q = warp & 3;
     const int part = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // key row == TMEM lane
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * kLog2e;
-    {  // K and V rows -> TMEM (this thread: key row r, quarter `part` of the D columns)
-      constexpr int CH = D / 32;  // 16-byte chunks per quarter row
-      uint32_t kv[4 * CH], vv[4 * CH];
-      mbar_wait(kv_full, 0);
+    int g = 0;
+    for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+      int bh, k0, nq;
+      decode(w, bh, k0, nq);
+      {  // K and V rows of item j -> TMEM (key row r, quarter `part` of the D columns)
+        constexpr int CH = D / 32;  // 16-byte chunks per quarter row
+        uint32_t kv[4 * CH], vv[4 * CH];
+        mbar_wait(kv_full, j & 1);
 #pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        const int cg = part * CH + i;
-        const uint32_t off = (cg >> 3) * C::KATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
-        const uint4 k4 = ld_shared_v4(base + C::K_OFF + off), v4 = ld_shared_v4(base + C::V_OFF + off);
-        kv[4 * i] = k4.x, kv[4 * i + 1] = k4.y, kv[4 * i + 2] = k4.z, kv[4 * i + 3] = k4.w;
-        vv[4 * i] = v4.x, vv[4 * i + 1] = v4.y, vv[4 * i + 2] = v4.z, vv[4 * i + 3] = v4.w;
-      }
-      if constexpr (CH == 4) {
-        tmem_st16(T_K + lo + part * 16, kv);
-        tmem_st16(T_V + lo + part * 16, vv);
-      } else {
-        tmem_st8(T_K + lo + part * 8, kv);
-        tmem_st8(T_V + lo + part * 8, vv);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      warp_arrive(kv_tmem);
-    }
-    for (int it = 0; it < nq; ++it) {
-      const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (it % C::QST) * 512) + part * 16;
-      if (threadIdx.x == 128) ZTRACE(1, 4, it);
-      mbar_wait(sp_full, it & 1);
-      if (threadIdx.x == 128) ZTRACE(1, 5, it);
-      tc_fence_after();
-#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (row threads only hand over)
-      tc_fence_before();
-      warp_arrive(sp_free);
-      if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);
-      warp_arrive(ds_full);
-      if (threadIdx.x == 128) ZTRACE(1, 7, it);
-      continue;
-#endif
-      uint32_t sv[16], pv[16];
-      tmem_ld16(T_S + lo + part * 16, sv);
-      tmem_ld16(T_DP + lo + part * 16, pv);
-      tmem_wait_ld();
-      tc_fence_before();
-      warp_arrive(sp_free);  // S^T(it+1) / dP^T(it+1) may now overwrite the buffers
-      float p[16], ds[16];
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(L + j);
-        const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + j);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          p[j + u] = fast_exp2(fmaf(__uint_as_float(sv[j + u]), sl2, -lv[u]));
-          ds[j + u] = dv[u] * scale;
+        for (int i = 0; i < CH; ++i) {
+          const int cg = part * CH + i;
+          const uint32_t off = (cg >> 3) * C::KATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
+          const uint4 k4 = ld_shared_v4(base + C::K_OFF + off), v4 = ld_shared_v4(base + C::V_OFF + off);
+          kv[4 * i] = k4.x, kv[4 * i + 1] = k4.y, kv[4 * i + 2] = k4.z, kv[4 * i + 3] = k4.w;
+          vv[4 * i] = v4.x, vv[4 * i + 1] = v4.y, vv[4 * i + 2] = v4.z, vv[4 * i + 3] = v4.w;
         }
+        if constexpr (CH == 4) {
+          tmem_st16(T_K + lo + part * 16, kv);
+          tmem_st16(T_V + lo + part * 16, vv);
+        } else {
+          tmem_st8(T_K + lo + part * 8, kv);
+          tmem_st8(T_V + lo + part * 8, vv);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(kv_tmem);
       }
-      if (it < 2) {  // tiles on the diagonal: key after query
-        const int qk = it * 64 + part * 16 - r;
+      for (int it = 0; it < nq; ++it, ++g) {
+        const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (g % C::QST) * 512) + part * 16;
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 4, it);
+        mbar_wait(sp_full, g & 1);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 5, it);
+        tc_fence_after();
+#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (row warps only hand over)
+        tc_fence_before();
+        warp_arrive(sp_free);
+        if (g >= 1) mbar_wait(ds_free, (g - 1) & 1);
+        warp_arrive(ds_full);
+        continue;
+#endif
+        uint32_t sv[16], pv[16];
+        tmem_ld16(T_S + lo + part * 16, sv);
+        tmem_ld16(T_DP + lo + part * 16, pv);
+        tmem_wait_ld();
+        tc_fence_before();
+        warp_arrive(sp_free);  // S^T / dP^T of the next tile may now overwrite the buffers
+        float p[16], ds[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (qk + j < 0) p[j] = 0.f;
+        for (int jj = 0; jj < 16; jj += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(L + jj);
+          const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + jj);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            p[jj + u] = fast_exp2(fmaf(__uint_as_float(sv[jj + u]), sl2, -lv[u]));
+            ds[jj + u] = dv[u] * scale;
+          }
+        }
+        if (it < 2) {  // tiles on the diagonal: key after query
+          const int qk = it * 64 + part * 16 - r;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (qk + jj < 0) p[jj] = 0.f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) ds[jj] = p[jj] * fmaf(__uint_as_float(pv[jj]), scale, -ds[jj]);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 6, it);
+        if (g >= 1) mbar_wait(ds_free, (g - 1) & 1);  // dV / dK of the previous tile done reading P^T / dS^T
+        const uint32_t rp = base + C::PT_OFF + r * 128, rd = base + C::DS_OFF + r * 128;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int c8 = part * 2 + t;
+          const float* pp = &p[t * 8];
+          const float* sd = &ds[t * 8];
+          const uint32_t sw = (c8 ^ (r & 7)) << 4;
+          st_shared_v4(rp + sw, pack_bf16(pp[0], pp[1]), pack_bf16(pp[2], pp[3]), pack_bf16(pp[4], pp[5]),
+                       pack_bf16(pp[6], pp[7]));
+          st_shared_v4(rd + sw, pack_bf16(sd[0], sd[1]), pack_bf16(sd[2], sd[3]), pack_bf16(sd[4], sd[5]),
+                       pack_bf16(sd[6], sd[7]));
+        }
+        fence_proxy_async();
+        warp_arrive(ds_full);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 7, it);
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) ds[j] = p[j] * fmaf(__uint_as_float(pv[j]), scale, -ds[j]);
-      if (threadIdx.x == 128) ZTRACE(1, 6, it);
-      if (it >= 1) mbar_wait(ds_free, (it - 1) & 1);  // dV / dK(it-1) done reading P^T / dS^T
-      const uint32_t rp = base + C::PT_OFF + r * 128, rd = base + C::DS_OFF + r * 128;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int c8 = part * 2 + t;
-        const float* pp = &p[t * 8];
-        const float* sd = &ds[t * 8];
-        const uint32_t sw = (c8 ^ (r & 7)) << 4;
-        st_shared_v4(rp + sw, pack_bf16(pp[0], pp[1]), pack_bf16(pp[2], pp[3]), pack_bf16(pp[4], pp[5]),
-                     pack_bf16(pp[6], pp[7]));
-        st_shared_v4(rd + sw, pack_bf16(sd[0], sd[1]), pack_bf16(sd[2], sd[3]), pack_bf16(sd[4], sd[5]),
-                     pack_bf16(sd[6], sd[7]));
+    }
+  } else if (warp >= 20) {
+    // epilogue warps: thread = TMEM lane (key row) r of quarter q, all D columns
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
+    for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+      int bh, k0, nq;
+      decode(w, bh, k0, nq);
+      const int b = bh / H, h = bh % H, row_base = b * T;
+      bool more = false;  // does this CTA take another item after this one?
+      for (int k2 = k + 1; k2 * (int)gridDim.x < nitems && !more; ++k2)
+        more = snake_item(k2, gridDim.x, blockIdx.x) < nitems;
+      mbar_wait(mm_done, j & 1);
+      // the staging area is the K / V smem: wait until K / V of the next item are in TMEM
+      if (more) mbar_wait(kv_tmem, (j + 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        stage_acc<32>(T_DK, lo, r, c, base + C::K_OFF);
+        stage_acc<32>(T_DV, lo, r, c, base + C::V_OFF);
       }
+      tc_fence_before();
+      warp_arrive(acc_free);  // dK / dV read: the MMA warp may start the next item's accumulation
       fence_proxy_async();
-      warp_arrive(ds_full);
-      if (threadIdx.x == 128) ZTRACE(1, 7, it);
-    }
-    mbar_wait(mm_done, 0);
-    if (threadIdx.x == 128) ZTRACE(1, 4, 63);
-    tc_fence_after();
-    // dK, dV -> swizzled smem tiles (the drained Q/dO ring) -> TMA stores
-    const uint32_t st_k = base + C::Q_OFF, st_v = st_k + C::KTILE;
-    stage_acc<D / 4>(T_DK, lo, r, part * (D / 4), st_k);
-    stage_acc<D / 4>(T_DV, lo, r, part * (D / 4), st_v);
-    fence_proxy_async();
-    named_bar_sync(1, 512);
-    if (threadIdx.x == 128) {
-      for (int a = 0; a < NA; ++a) {
-        tma_store_2d(&tm_st, st_k + a * C::KATOM, H * D + h * D + 64 * a, row_base + k0);
-        tma_store_2d(&tm_st, st_v + a * C::KATOM, 2 * H * D + h * D + 64 * a, row_base + k0);
+      named_bar_sync(2, 128);
+      if (threadIdx.x == 640) {
+        for (int a = 0; a < NA; ++a) {
+          tma_store_2d(&tm_st, base + C::K_OFF + a * C::KATOM, H * D + h * D + 64 * a, row_base + k0);
+          tma_store_2d(&tm_st, base + C::V_OFF + a * C::KATOM, 2 * H * D + h * D + 64 * a, row_base + k0);
+        }
+        bulk_commit();
+        bulk_wait_all();
+        mbar_arrive(kv_empty);  // staging smem free: the producer may load K / V of item j+2
+        if (j == 0) ZTRACE(1, 5, 63);
       }
-      bulk_commit();
-      bulk_wait_all();
+      if (threadIdx.x == 640 && j == 0) ZTRACE(1, 4, 63);
     }
-    if (threadIdx.x == 128) ZTRACE(1, 5, 63);
   }
   tc_fence_before();
   __syncthreads();
@@ -715,16 +853,18 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
   float* delta = ws;
   float* lse2 = ws + (long long)BH * T;
   const float scale = 1.f / sqrtf((float)D);
-  const dim3 grid((T / 128) * BH);
-  attn_bwd_dq_kernel<D><<<grid, 384, BwdDqCfg<D>::SMEM, s>>>(m_q128, m_kv64, m_do128, m_st, (const bf16*)out, lse, delta, lse2,
-                                                               (bf16*)dqkv, T, H, BH, scale);
+  const int items = (T / 128) * BH;
+  const dim3 pgrid(items < num_sms() ? items : num_sms());  // persistent kernels: one CTA per SM
+  attn_bwd_dq_kernel<D><<<pgrid, BwdDqCfg<D>::THREADS, BwdDqCfg<D>::SMEM, s>>>(m_q128, m_kv64, m_do128, m_st,
+                                                                             (const bf16*)out, lse, delta, lse2, T, H,
+                                                                             BH, scale);
   rc = check_launch("attn_bwd_dq");
   if (rc) return rc;
   // dK/dV launched as a programmatic dependent of the dQ kernel: its prologue (TMEM, barriers,
   // K/V/Q/dO loads) runs on SMs the dQ tail leaves idle; only the lse2 / delta loads wait
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(640);
+  cfg.gridDim = pgrid;
+  cfg.blockDim = dim3(BwdDkdvCfg<D>::THREADS);
   cfg.dynamicSmemBytes = BwdDkdvCfg<D>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -733,7 +873,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, m_st, (const float*)lse2,
-                                     (const float*)delta, (bf16*)dqkv, T, H, BH, scale);
+                                     (const float*)delta, T, H, BH, scale);
   if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv launch");
   return check_launch("attn_bwd_dkdv");
 }
