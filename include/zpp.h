@@ -131,6 +131,8 @@ int zpp_xent_fwd_bwd(void* logits, long long ld, const int64_t* labels, float* l
 /* ---- ZeRO gradient path (RS_GRAD, schedules.py:76-78) --------------------------- */
 int zpp_cast_scale_f32_bf16(const float* in, void* out, long long n, float scale, uintptr_t stream);
 int zpp_accum_bf16_f32(const void* in, float* acc, long long n, uintptr_t stream);
+/* acc += in, both fp32 (the fp32-wire variant of RS_GRAD, Runtime(rs_wire="fp32")); n % 4 == 0 */
+int zpp_accum_f32_f32(const float* in, float* acc, long long n, uintptr_t stream);
 
 /* ---- sharded AdamW (OPT, schedules.py:89-91) ----------------------------------- */
 int zpp_adamw(float* master, float* exp_avg, float* exp_avg_sq, const float* grad, void* param_bf16, long long n,

@@ -601,6 +601,16 @@ __global__ void cast_scale_kernel(const float* __restrict__ in, bf16* __restrict
   }
 }
 
+// acc += in (fp32 wire of the gradient reduce-scatter, Runtime(rs_wire="fp32"))
+__global__ void accum_f32_kernel(const float4* __restrict__ in, float4* __restrict__ acc, long long nvec) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    const float4 x = in[i];
+    float4 a = acc[i];
+    a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+    acc[i] = a;
+  }
+}
+
 __global__ void accum_kernel(const bf16* __restrict__ in, float* __restrict__ acc, long long nvec) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
     float f[8];
@@ -678,7 +688,7 @@ int kernels_preload() {
                        (const void*)swiglu_fwd_kernel, (const void*)swiglu_bwd_kernel, (const void*)rope_kernel,
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_wte_kernel, (const void*)embed_bwd_wpe_kernel,
-                       (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel,
+                       (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel, (const void*)accum_f32_kernel,
                        (const void*)adamw_kernel, (const void*)init_param_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&fa, f);
@@ -866,6 +876,15 @@ extern "C" int zpp_accum_bf16_f32(const void* in, float* acc, long long n, uintp
   if (n % 8) return set_error(ZPP_ERR_ARG, "accum: n % 8 != 0");
   accum_kernel<<<grid_for(n / 8, 256), 256, 0, STREAM(stream)>>>((const bf16*)in, acc, n / 8);
   return check_launch("accum");
+}
+
+extern "C" int zpp_accum_f32_f32(const float* in, float* acc, long long n, uintptr_t stream) {
+  if (n % 4) return set_error(ZPP_ERR_ARG, "accum_f32: n % 4 != 0");
+  if (n == 0) return ZPP_OK;
+  const long long nvec = n / 4;
+  accum_f32_kernel<<<grid_for(nvec, 256), 256, 0, STREAM(stream)>>>(reinterpret_cast<const float4*>(in),
+                                                                     reinterpret_cast<float4*>(acc), nvec);
+  return check_launch("accum_f32");
 }
 
 extern "C" int zpp_adamw(float* master, float* exp_avg, float* exp_avg_sq, const float* grad, void* param_bf16,

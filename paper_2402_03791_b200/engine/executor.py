@@ -187,12 +187,18 @@ class Runtime:
     def __init__(self, spec: GPTSpec, model: ModelSpec, cfg: ParallelConfig, placement: Placement,
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
-                 aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True):
+                 aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True,
+                 rs_wire: str = "bf16"):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
         (first two steps, debugging); ``memory_check``: refuse configurations whose estimated
-        peak does not fit (see below)."""
+        peak does not fit (see below); ``rs_wire``: "bf16" (the reference's byte model,
+        `schedules.py:76-78`) or "fp32" (RS_GRAD sums in fp32 on the wire: twice the bytes, no
+        bf16 rounding of the partial sums -- tools/rs_wire_drift.py measures the difference)."""
+        if rs_wire not in ("bf16", "fp32"):
+            raise ValueError("rs_wire must be 'bf16' or 'fp32'")
+        self.rs_wire = rs_wire
         if world != cfg.pp_size * cfg.dp_size * cfg.inter_node_dp:
             raise ValueError(f"world size {world} != n*P*D = "
                              f"{cfg.inter_node_dp * cfg.pp_size * cfg.dp_size}")
@@ -274,6 +280,8 @@ class Runtime:
         if self.D > 1 or self.n > 1:
             self.rs_send = torch.empty(max_n, dtype=BF16, device=self.dev)
             self.rs_recv = torch.empty(max_ns, dtype=BF16, device=self.dev)
+            if self.rs_wire == "fp32" and self.D > 1:  # intra-group RS sums fp32 grad_full directly
+                self.rs_recv32 = torch.empty(max_ns, dtype=F32, device=self.dev)
         self.loss_sum = torch.zeros(1, dtype=F32, device=self.dev)
         self.step_count = 0
         self.opt_event = None
@@ -517,15 +525,25 @@ class Runtime:
         self._join_aux(rs)                           # ... and their parameter-grad reductions
         self._begin(rs)
         n, ns = st.lay.numel, st.lay.shard_numel
-        send, recv = self.rs_send[:n], self.rs_recv[:ns]
-        ops.cast_scale(st.grad_full, send, 1.0, stream=rs)
-        st.zero_scatter_grads(rs)
-        st.new_window()
-        st.grad_free_event = self._record(rs)
-        lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], send.data_ptr(), recv.data_ptr(), ns, 0,
-                 rs.cuda_stream)
-        self.nccl_bytes["intra"] += (self.D - 1) * ns * 2
-        ops.accum(recv, st.grad_shard, stream=rs)
+        if self.rs_wire == "fp32":  # the fp32 stage grad IS the send buffer: reduce, then release it
+            recv = self.rs_recv32[:ns]
+            lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], st.grad_full.data_ptr(), recv.data_ptr(), ns,
+                     1, rs.cuda_stream)
+            self.nccl_bytes["intra"] += (self.D - 1) * ns * 4
+            st.zero_scatter_grads(rs)
+            st.new_window()
+            st.grad_free_event = self._record(rs)
+            ops.accum_f32(recv, st.grad_shard, stream=rs)
+        else:
+            send, recv = self.rs_send[:n], self.rs_recv[:ns]
+            ops.cast_scale(st.grad_full, send, 1.0, stream=rs)
+            st.zero_scatter_grads(rs)
+            st.new_window()
+            st.grad_free_event = self._record(rs)
+            lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], send.data_ptr(), recv.data_ptr(), ns, 0,
+                     rs.cuda_stream)
+            self.nccl_bytes["intra"] += (self.D - 1) * ns * 2
+            ops.accum(recv, st.grad_shard, stream=rs)
         ev = self._record(rs)
         self._rs_events.append(ev)
         if self.early_opt and self._final_rs.get(s) == self._ti:

@@ -45,6 +45,7 @@ _SIGS = {
     "zpp_xent_fwd_bwd": (c_int, [P, c_size, P, P, c_int, c_int, c_float, c_stream]),
     "zpp_cast_scale_f32_bf16": (c_int, [P, P, c_size, c_float, c_stream]),
     "zpp_accum_bf16_f32": (c_int, [P, P, c_size, c_stream]),
+    "zpp_accum_f32_f32": (c_int, [P, P, c_size, c_stream]),
     "zpp_adamw": (c_int, [P, P, P, P, P, c_size, c_float, c_float, c_float, c_float, c_float, c_int,
                           c_stream]),
     "zpp_init_param": (c_int, [P, P, c_size, c_ulonglong, c_size, c_float, c_float, c_stream]),

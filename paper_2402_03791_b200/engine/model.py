@@ -247,13 +247,14 @@ def shard_init_ranges(lay: StageLayout, z: int):
             yield slot, a - slot.offset, a - lo, b - a
 
 
-def nccl_bytes_per_step(spec: GPTSpec, cfg, placement, sched, p: int) -> tuple[int, int]:
+def nccl_bytes_per_step(spec: GPTSpec, cfg, placement, sched, p: int, rs_wire: str = "bf16") -> tuple[int, int]:
     """(intra, inter) bytes pipeline rank ``p`` receives through NCCL in one step, task by task
     as the executor issues them (ring collectives: an all-gather / reduce-scatter over g ranks
     moves (g-1)/g of the full buffer per rank, an all-reduce twice that):
 
     * AG_PARAM, RS_GRAD (`schedules.py:72-78`): (D-1) x shard x 2 B of the stage's flat bf16
-      buffer -- the reference's ``((D-1)/D) * M_w * layers`` with the stage's real size;
+      buffer -- the reference's ``((D-1)/D) * M_w * layers`` with the stage's real size
+      (RS_GRAD x 4 B with ``rs_wire="fp32"``);
     * AR_GRAD (`:80-81`): 2 (n-1)/n x shard x 2 B per local stage;
     * RS_GRAD_INTER / AG_PARAM_INTER (`:83-87`): (n-1) x optimizer sub-shard x 2 B per stage.
     ``StepResult.nccl_bytes_intra/inter`` must equal this (tests/test_engine_gpu.py via
@@ -264,8 +265,10 @@ def nccl_bytes_per_step(spec: GPTSpec, cfg, placement, sched, p: int) -> tuple[i
     lays = {s: stage_layout(spec, s, S, placement.stage_to_layers[s], D, sub) for s in placement.device_stages(p)}
     intra = inter = 0
     for t in sched.per_device[p]:
-        if t.kind in (TaskKind.AG_PARAM, TaskKind.RS_GRAD):
+        if t.kind is TaskKind.AG_PARAM:
             intra += (D - 1) * lays[t.stage].shard_numel * 2
+        elif t.kind is TaskKind.RS_GRAD:
+            intra += (D - 1) * lays[t.stage].shard_numel * (4 if rs_wire == "fp32" else 2)
         elif t.kind is TaskKind.AR_GRAD and n > 1:
             inter += sum(2 * (n - 1) * lay.shard_numel * 2 // n for lay in lays.values())
         elif t.kind in (TaskKind.RS_GRAD_INTER, TaskKind.AG_PARAM_INTER) and n > 1:

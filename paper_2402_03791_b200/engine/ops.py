@@ -237,6 +237,14 @@ def accum(src_bf16, acc_f32, stream=None):
     lib.call("zpp_accum_bf16_f32", _p(src_bf16), _p(acc_f32), src_bf16.numel(), _s(stream))
 
 
+def accum_f32(src_f32, acc_f32, stream=None):
+    """acc += src (fp32); the fp32-wire reduce-scatter's accumulate."""
+    if src_f32.numel() != acc_f32.numel():
+        raise ValueError("accum_f32: size mismatch")
+    _count(1)
+    lib.call("zpp_accum_f32_f32", _p(src_f32), _p(acc_f32), src_f32.numel(), _s(stream))
+
+
 def adamw(master, m, v, grad, param_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
     n = master.numel()
     if not (m.numel() == v.numel() == grad.numel() == param_bf16.numel() == n):

@@ -1,6 +1,6 @@
 """One rank of a multi-GPU ZeroPP step under torchrun; compares its shards with the oracle.
 
-usage: torchrun --nproc-per-node n*P*D dist_worker.py P D B U V OUTDIR [n MODE]
+usage: torchrun --nproc-per-node n*P*D dist_worker.py P D B U V OUTDIR [n MODE [RS_WIRE]]
 
 n = inter_node_dp replicas emulated on one box, MODE = dp_outer | zero1_outer.
 """
@@ -27,6 +27,7 @@ def main():
     out = sys.argv[6]
     n = int(sys.argv[7]) if len(sys.argv) > 7 else 1
     mode = sys.argv[8] if len(sys.argv) > 8 else "dp_outer"
+    rs_wire = sys.argv[9] if len(sys.argv) > 9 else "bf16"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("gloo")
@@ -35,7 +36,8 @@ def main():
     try:
         rt, (model, cfg, pl, sched), tokens, res = run_engine_step(spec, P, D, B, U, V, rank=rank, world=world,
                                                                     inter_node_dp=n,
-                                                                    hybrid_mode=HybridMode(mode))
+                                                                    hybrid_mode=HybridMode(mode),
+                                                                    rt_kw={"rs_wire": rs_wire})
         loss_sum = torch.tensor([res[0].loss_sum.item()])
         dist.all_reduce(loss_sum)
         loss = loss_sum.item() / (n * D * B * spec.tokens_per_microbatch)
@@ -47,7 +49,7 @@ def main():
         elif not all(0 < b <= sim.makespan for b in sim.per_device_busy):
             fails.append(f"measured busy/makespan inconsistent: {sim.per_device_busy} / {sim.makespan}")
         from paper_2402_03791_b200.engine.model import nccl_bytes_per_step
-        want = nccl_bytes_per_step(spec, cfg, pl, sched, rt.p)
+        want = nccl_bytes_per_step(spec, cfg, pl, sched, rt.p, rs_wire=rs_wire)
         got = (res[0].nccl_bytes_intra, res[0].nccl_bytes_inter)
         if got != want:
             fails.append(f"NCCL bytes {got} != planned {want}")

@@ -104,12 +104,13 @@ def test_loss_decreases_over_steps():
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs (run via gpurun --gpus 4)")
-@pytest.mark.parametrize("P,D,B,U,V", [(2, 2, 8, 4, 2), (4, 1, 8, 4, 1), (1, 4, 4, 2, 2)])
-def test_multi_gpu_step_matches_oracle(tmp_path, P, D, B, U, V):
+@pytest.mark.parametrize("P,D,B,U,V,wire", [(2, 2, 8, 4, 2, "bf16"), (4, 1, 8, 4, 1, "bf16"), (1, 4, 4, 2, 2, "bf16"),
+                                            (2, 2, 8, 4, 2, "fp32"), (1, 4, 4, 2, 2, "fp32")])
+def test_multi_gpu_step_matches_oracle(tmp_path, P, D, B, U, V, wire):
     here = os.path.dirname(os.path.abspath(__file__))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P * D}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(here, "dist_worker.py"),
-           str(P), str(D), str(B), str(U), str(V), str(tmp_path)]
+           str(P), str(D), str(B), str(U), str(V), str(tmp_path), "1", "dp_outer", wire]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for rank in range(P * D):
