@@ -188,7 +188,7 @@ class Runtime:
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
                  aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True,
-                 rs_wire: str = "bf16"):
+                 rs_wire: str = "bf16", stream_priority: bool = True):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
@@ -240,12 +240,17 @@ class Runtime:
         for s in self.local_stages:
             lay = stage_layout(spec, s, self.S, placement.stage_to_layers[s], self.D, self.sub)
             self.stages[s] = _Stage(lay, self.D, self.z, self.dev, self.sub, self.node)
-        mk = lambda: torch.cuda.Stream(device=self.dev)  # noqa: E731
+        # Stream priorities: the block scheduler fills freed SMs from higher-priority streams
+        # first.  The critical path (compute, collectives, P2P) is high priority; the side
+        # streams (aux column reductions, early AdamW) only soak up idle SMs (stream_priority
+        # = False gives every stream the default priority).
+        hi = torch.cuda.Stream.priority_range()[1] if stream_priority else 0
+        mk = lambda prio=hi: torch.cuda.Stream(device=self.dev, priority=prio)  # noqa: E731
         self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
         self.s_act_send, self.s_act_recv, self.s_grad_send, self.s_grad_recv = mk(), mk(), mk(), mk()
         # parameter-gradient column reductions (bias, norm gamma / beta) only feed RS / OPT:
         # they run on this side stream beside the next GEMMs (aux_stream=False keeps them inline)
-        self.s_aux = mk() if aux_stream else self.s_comp
+        self.s_aux = mk(0) if aux_stream else self.s_comp
         # Early optimizer: a stage's AdamW starts on its own stream as soon as the stage's
         # gradients are final (its last W at D == 1, layer by layer; its last RS_GRAD at
         # D > 1), overlapping the remaining B / W work instead of trailing the step.  The OPT
@@ -254,7 +259,7 @@ class Runtime:
         # at D == 1 there is nothing to overlap but the GEMMs, which under the power cap only
         # slows them (measured: profiles/r01c_ab_n1_aux_earlyopt_b2.txt), so it is off there.
         self.early_opt = self.n == 1 and (self.D > 1 if early_opt is None else bool(early_opt))
-        self.s_opt = mk()
+        self.s_opt = mk(0)
         # CUDA-graph mode (cuda_graph=True; one rank, no early optimizer): the task list up to
         # OPT is captured once, on the second step, and replayed; OPT runs eagerly after it
         # (AdamW's bias correction depends on the step number).  Shapes, buffers and the task

@@ -24,7 +24,7 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
 dist.init_process_group("gloo")
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-B = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 spec = GPTSpec(num_layers=L, hidden=4096, heads=32, seq_len=2048, microbatch_samples=2)
 out = {}
 for wire in ("bf16", "fp32"):
@@ -33,8 +33,9 @@ for wire in ("bf16", "fp32"):
     out[wire] = {s: rt.captured[s].float().clone() for s in rt.stages}
     lo = rt.z * rt.stages[0].lay.shard_numel
     ns = rt.stages[0].lay.shard_numel
-    del rt
+    del rt, res
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 # oracle params: the deterministic init, gathered from the numpy restatement (small: 2 layers)
 from engine_harness import oracle_params  # noqa: E402
 params = oracle_params(spec, cfg, pl)
