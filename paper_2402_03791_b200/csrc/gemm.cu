@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const bool leader = crank == 0;
 
   if (threadIdx.x == 0) {
+    // every CTA of this persistent grid is resident: let the next kernel's CTAs launch as ours exit
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
@@ -246,6 +248,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch (the launch sets ProgrammaticStreamSerialization): this CTA's
+  // launch and prologue above overlapped the previous kernel's tail; everything below (the
+  // tile counter the previous GEMM re-arms, operands, residuals) waits for it to complete.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int num_m = (M + TILE_M - 1) / TILE_M;
   const int num_n = (N + BN - 1) / BN;
@@ -739,13 +745,15 @@ static int launch_gemm(const void* A, long long lda, const void* B, long long ld
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   unsigned* sched = sched_slot(stream);
   if (!sched)
     return set_error(ZPP_ERR_ARG, g_sched ? "gemm: more than 32 launching streams"

@@ -188,7 +188,7 @@ class Runtime:
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
                  aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True,
-                 rs_wire: str = "bf16", stream_priority: bool = True):
+                 rs_wire: str = "bf16", stream_priority: bool = False):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
@@ -240,10 +240,10 @@ class Runtime:
         for s in self.local_stages:
             lay = stage_layout(spec, s, self.S, placement.stage_to_layers[s], self.D, self.sub)
             self.stages[s] = _Stage(lay, self.D, self.z, self.dev, self.sub, self.node)
-        # Stream priorities: the block scheduler fills freed SMs from higher-priority streams
-        # first.  The critical path (compute, collectives, P2P) is high priority; the side
-        # streams (aux column reductions, early AdamW) only soak up idle SMs (stream_priority
-        # = False gives every stream the default priority).
+        # stream_priority=True: the critical path (compute, collectives, P2P) gets the highest
+        # stream priority, the side streams (aux column reductions, early AdamW) the lowest, so
+        # the block scheduler fills freed SMs from the critical path first.  Off by default:
+        # neutral to -0.4% at N=1 (tools/step_ab.py, profiles/r02/step_ab_priority.txt).
         hi = torch.cuda.Stream.priority_range()[1] if stream_priority else 0
         mk = lambda prio=hi: torch.cuda.Stream(device=self.dev, priority=prio)  # noqa: E731
         self.s_comp, self.s_ag, self.s_rs = mk(), mk(), mk()
