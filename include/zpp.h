@@ -92,16 +92,6 @@ long long zpp_layernorm_bwd_workspace_floats(int rows, int cols);
 int zpp_norm_param_grads(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma,
                          float* dbeta, float* workspace, int rows, int cols, int accumulate, uintptr_t stream);
 
-/* LayerNorm (mean != NULL) / RMSNorm (mean == NULL) backward with the parameter gradients folded
- * in: dx as zpp_layernorm_bwd / zpp_rmsnorm_bwd, and dgamma (+dbeta for LayerNorm) (+)= their
- * column sums -- per-block register partials (partials: zpp_norm_bwd_fused_partials_floats
- * floats, no initialisation needed) summed in block order by a second small kernel, so x and dy
- * are read once.  Deterministic.  cols % 8 == 0, cols <= 4096. */
-int zpp_norm_bwd_fused(const void* dy, const void* x, const float* mean, const float* rstd, const void* gamma,
-                       const void* dresid, void* dx, float* dgamma, float* dbeta, float* partials, int rows, int cols,
-                       int accumulate, uintptr_t stream);
-long long zpp_norm_bwd_fused_partials_floats(int rows, int cols);
-
 /* ---- LLaMA block pieces: RMSNorm, SwiGLU, rotary embedding ----------------------- */
 /* y = x * rstd * gamma, rstd = 1/sqrt(mean(x^2) + eps) (fp32 rstd out, [rows]) */
 int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols, float eps,

@@ -192,131 +192,6 @@ __global__ void __launch_bounds__(128) layernorm_bwd_dx_pk_kernel(const bf16* __
   }
 }
 
-// Backward with the parameter gradients folded in (rows of <= 4096 columns): a grid of G
-// blocks, block b takes rows b, b + G, ... and, besides dx (same math as the packed kernel
-// above), accumulates its rows' dgamma = sum dy*xhat and dbeta = sum dy per column in
-// registers (thread = 8*LN_VPT fixed columns), then writes one partial row pair per block.
-// norm_partials_reduce_kernel sums the G partials of each column in block order
-// (deterministic).  This replaces the separate column-reduction pass over x and dy (2*h*T
-// bytes read again on the side stream) by G*2*h*4 bytes of partials.
-template <bool RMS>
-__global__ void __launch_bounds__(128) layernorm_bwd_fused_kernel(const bf16* __restrict__ dy,
-                                                                  const bf16* __restrict__ x,
-                                                                  const float* __restrict__ mean,
-                                                                  const float* __restrict__ rstd,
-                                                                  const bf16* __restrict__ g,
-                                                                  const bf16* __restrict__ dres,
-                                                                  bf16* __restrict__ dx, float* __restrict__ part,
-                                                                  int rows, int cols) {
-  constexpr int NT = 128;
-  __shared__ float2 red[2][NT / 32];
-  const int nvec = cols / 8;
-  float ga[LN_VPT][8], ba[LN_VPT][8];
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) ga[i][j] = ba[i][j] = 0.f;
-  int par = 0;
-  for (int row = blockIdx.x; row < rows; row += gridDim.x, par ^= 1) {
-    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
-    const bf16* xr = x + (long long)row * cols;
-    const bf16* dyr = dy + (long long)row * cols;
-    uint4 xw[LN_VPT], dw[LN_VPT], rv[LN_VPT];
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * NT;
-      if (vi < nvec) {
-        xw[i] = ld_na(xr + vi * 8);
-        dw[i] = ld_na(dyr + vi * 8);
-        if (dres) rv[i] = ld_na(dres + (long long)row * cols + vi * 8);
-      }
-    }
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * NT;
-      if (vi < nvec) {
-        float xv[8], dv[8], gv[8];
-        unpack8(xw[i], xv);
-        unpack8(dw[i], dv);
-        unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float xh = (xv[j] - mu) * rs, dg = dv[j] * gv[j];
-          s1 += dg;
-          s2 += dg * xh;
-          ga[i][j] += dv[j] * xh;
-          ba[i][j] += dv[j];
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) red[par][w] = make_float2(s1, s2);  // double-buffered: one barrier per row
-    __syncthreads();
-    float2 t = red[par][0];
-#pragma unroll
-    for (int i = 1; i < NT / 32; ++i) { t.x += red[par][i].x; t.y += red[par][i].y; }
-    const float m1 = RMS ? 0.f : t.x / cols, m2 = t.y / cols;
-    bf16* dxr = dx + (long long)row * cols;
-#pragma unroll
-    for (int i = 0; i < LN_VPT; ++i) {
-      const int vi = threadIdx.x + i * NT;
-      if (vi < nvec) {
-        float xv[8], dv[8], gv[8], o[8];
-        unpack8(xw[i], xv);
-        unpack8(dw[i], dv);
-        unpack8(*reinterpret_cast<const uint4*>(g + vi * 8), gv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float xh = (xv[j] - mu) * rs, dg = dv[j] * gv[j];
-          o[j] = rs * (dg - m1 - xh * m2);
-        }
-        if (dres) {
-          float r[8];
-          unpack8(rv[i], r);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] += r[j];
-        }
-        *reinterpret_cast<uint4*>(dxr + vi * 8) = pack8(o);
-      }
-    }
-  }
-  float* pg = part + (long long)blockIdx.x * 2 * cols;  // [G][2][cols]: dgamma row, dbeta row
-#pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    const int vi = threadIdx.x + i * NT;
-    if (vi < nvec) {
-      float4* a = reinterpret_cast<float4*>(pg + vi * 8);
-      a[0] = make_float4(ga[i][0], ga[i][1], ga[i][2], ga[i][3]);
-      a[1] = make_float4(ga[i][4], ga[i][5], ga[i][6], ga[i][7]);
-      if (!RMS) {
-        float4* c = reinterpret_cast<float4*>(pg + cols + vi * 8);
-        c[0] = make_float4(ba[i][0], ba[i][1], ba[i][2], ba[i][3]);
-        c[1] = make_float4(ba[i][4], ba[i][5], ba[i][6], ba[i][7]);
-      }
-    }
-  }
-}
-
-// out0[c] (+)= sum_b part[b][0][c], out1[c] (+)= sum_b part[b][1][c], b in block order.
-__global__ void norm_partials_reduce_kernel(const float* __restrict__ part, float* __restrict__ out0,
-                                            float* __restrict__ out1, int nblocks, int cols, int accumulate) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float s0 = 0.f, s1 = 0.f;
-  for (int b = 0; b < nblocks; ++b) {
-    s0 += __ldcg(part + (long long)b * 2 * cols + c);
-    if (out1) s1 += __ldcg(part + (long long)b * 2 * cols + cols + c);
-  }
-  out0[c] = accumulate ? out0[c] + s0 : s0;
-  if (out1) out1[c] = accumulate ? out1[c] + s1 : s1;
-}
-
 // dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) (+ dresid); one row per block,
 // the two row sums fused into a single float2 block reduction.  RMS: mean = 0 and the
 // mean(dy*g) term drops (xhat = x * rstd).
@@ -814,8 +689,6 @@ int kernels_preload() {
                        (const void*)colred_kernel<true>, (const void*)colred_kernel<false>,
                        (const void*)gelu_kernel, (const void*)embed_fwd_kernel, (const void*)embed_bwd_wte_kernel, (const void*)embed_bwd_wpe_kernel,
                        (const void*)xent_kernel, (const void*)cast_scale_kernel, (const void*)accum_kernel, (const void*)accum_f32_kernel,
-                       (const void*)layernorm_bwd_fused_kernel<false>, (const void*)layernorm_bwd_fused_kernel<true>,
-                       (const void*)norm_partials_reduce_kernel,
                        (const void*)adamw_kernel, (const void*)init_param_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&fa, f);
@@ -883,38 +756,6 @@ extern "C" int zpp_layernorm_bwd(const void* dy, const void* x, const float* mea
   if (rc || !dgamma) return rc;  // dgamma == null: parameter grads via zpp_norm_param_grads
   return colred_launch(true, dy, cols, x, mean, rstd, dgamma, dbeta, workspace, rows, cols, accumulate,
                        STREAM(stream));
-}
-
-static int ln_fused_blocks(int rows) {
-  const int g = 2 * num_sms();
-  return rows < g ? rows : g;
-}
-
-extern "C" long long zpp_norm_bwd_fused_partials_floats(int rows, int cols) {
-  return (long long)ln_fused_blocks(rows) * 2 * cols;
-}
-
-// LayerNorm (mean != NULL) / RMSNorm (mean == NULL) backward with dgamma / dbeta folded in.
-extern "C" int zpp_norm_bwd_fused(const void* dy, const void* x, const float* mean, const float* rstd,
-                                  const void* gamma, const void* dresid, void* dx, float* dgamma, float* dbeta,
-                                  float* partials, int rows, int cols, int accumulate, uintptr_t stream) {
-  if (cols % 8 || cols > 128 * 8 * LN_VPT) return set_error(ZPP_ERR_ARG, "norm_bwd_fused: cols % 8 != 0 or > 4096");
-  if (!partials || !dgamma) return set_error(ZPP_ERR_ARG, "norm_bwd_fused: partials and dgamma required");
-  if (rows <= 0) return ZPP_OK;
-  const int G = ln_fused_blocks(rows);
-  if (mean)
-    layernorm_bwd_fused_kernel<false><<<G, 128, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, mean, rstd,
-                                                                     (const bf16*)gamma, (const bf16*)dresid,
-                                                                     (bf16*)dx, partials, rows, cols);
-  else
-    layernorm_bwd_fused_kernel<true><<<G, 128, 0, STREAM(stream)>>>((const bf16*)dy, (const bf16*)x, nullptr, rstd,
-                                                                    (const bf16*)gamma, (const bf16*)dresid,
-                                                                    (bf16*)dx, partials, rows, cols);
-  int rc = check_launch("norm_bwd_fused");
-  if (rc) return rc;
-  norm_partials_reduce_kernel<<<(cols + 255) / 256, 256, 0, STREAM(stream)>>>(partials, dgamma, mean ? dbeta : nullptr,
-                                                                               G, cols, accumulate);
-  return check_launch("norm_partials_reduce");
 }
 
 extern "C" int zpp_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int rows, int cols, float eps,

@@ -188,7 +188,7 @@ class Runtime:
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
                  aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True,
-                 rs_wire: str = "bf16", stream_priority: bool = False, fused_norm_bwd: bool = True):
+                 rs_wire: str = "bf16", stream_priority: bool = False):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
@@ -196,7 +196,6 @@ class Runtime:
         peak does not fit (see below); ``rs_wire``: "bf16" (the reference's byte model,
         `schedules.py:76-78`) or "fp32" (RS_GRAD sums in fp32 on the wire: twice the bytes, no
         bf16 rounding of the partial sums -- tools/rs_wire_drift.py measures the difference)."""
-        self.fused_norm_bwd = fused_norm_bwd and spec.hidden <= 4096
         if rs_wire not in ("bf16", "fp32"):
             raise ValueError("rs_wire must be 'bf16' or 'fp32'")
         self.rs_wire = rs_wire
@@ -277,8 +276,6 @@ class Runtime:
         T, h = spec.tokens_per_microbatch, spec.hidden
         # column-reduction workspaces carry re-armed tickets: zero them once
         self.ln_ws = torch.zeros(ops.layernorm_bwd_workspace(T, h), dtype=F32, device=self.dev)
-        self.norm_part = (torch.empty(ops.norm_bwd_fused_partials(T, h), dtype=F32, device=self.dev)
-                          if self.fused_norm_bwd else None)
         self.cs_ws = torch.zeros(ops.colsum_workspace(T, 4 * h), dtype=F32, device=self.dev)
         self.attn_ws = torch.empty(ops.attn_bwd_workspace(spec.microbatch_samples, spec.seq_len,
                                                           spec.heads, spec.head_dim),
@@ -756,16 +753,8 @@ class Runtime:
             stream.wait_event(self._record(self.s_aux))
 
     def _norm_bwd(self, st: "_Stage", dy, x, mean, rstd, gkey, bkey, dx, dresid=None) -> None:
-        """LayerNorm (mean given) / RMSNorm backward.  fused_norm_bwd: dx and the gamma / beta grads
-        in one pass on compute (x, dy read once); else dx on compute, gamma / beta grads on aux."""
+        """LayerNorm (mean given) / RMSNorm backward: dx on compute, gamma / beta grads on aux."""
         P, G = st.p, st.g
-        if self.fused_norm_bwd:
-            acc = st.accumulate(gkey)
-            if bkey is not None:
-                acc = acc | st.accumulate(bkey)
-            ops.norm_bwd_fused(dy, x, mean, rstd, P[gkey], dx, G[gkey], G[bkey] if bkey is not None else None,
-                               self.norm_part, dresid=dresid, accumulate=acc)
-            return
         if mean is None:
             ops.rmsnorm_bwd(dy, x, rstd, P[gkey], dx, None, None, dresid=dresid)
         else:

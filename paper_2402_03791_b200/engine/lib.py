@@ -33,8 +33,6 @@ _SIGS = {
     "zpp_layernorm_bwd": (c_int, [P, P, P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_layernorm_bwd_workspace_floats": (c_longlong, [c_int, c_int]),
     "zpp_norm_param_grads": (c_int, [P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
-    "zpp_norm_bwd_fused": (c_int, [P, P, P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
-    "zpp_norm_bwd_fused_partials_floats": (c_longlong, [c_int, c_int]),
     "zpp_rmsnorm_fwd": (c_int, [P, P, P, P, c_int, c_int, c_float, c_stream]),
     "zpp_rmsnorm_bwd": (c_int, [P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_stream]),
     "zpp_swiglu_fwd": (c_int, [P, P, c_int, c_int, c_stream]),

@@ -135,19 +135,6 @@ def norm_param_grads(dy, x, mean, rstd, dgamma, dbeta, workspace, accumulate=Tru
              rows, cols, int(accumulate), _s(stream))
 
 
-def norm_bwd_fused_partials(rows: int, cols: int) -> int:
-    return lib.load().zpp_norm_bwd_fused_partials_floats(rows, cols)
-
-
-def norm_bwd_fused(dy, x, mean, rstd, gamma, dx, dgamma, dbeta, partials, dresid=None, accumulate=True, stream=None):
-    """LayerNorm (mean given) / RMSNorm (mean None) backward with dgamma / dbeta (+)= folded in
-    (x and dy read once; deterministic block-order partial sums)."""
-    rows, cols = x.shape
-    _count(2)
-    lib.call("zpp_norm_bwd_fused", _p(dy), _p(x), _p(mean), _p(rstd), _p(gamma), _p(dresid), _p(dx), _p(dgamma),
-             _p(dbeta), _p(partials), rows, cols, int(accumulate), _s(stream))
-
-
 def rmsnorm_fwd(x, gamma, y, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
     _count(1)

@@ -13,7 +13,6 @@ x, g, b, dy, dres = bf(T, h), bf(h), bf(h), bf(T, h), bf(T, h)
 y, dx = torch.empty_like(x), torch.empty_like(x)
 mean, rstd = torch.empty(T, device=dev), torch.empty(T, device=dev)
 ws = torch.zeros(ops.layernorm_bwd_workspace(T, 4 * h), device=dev)
-part = torch.empty(ops.norm_bwd_fused_partials(T, h), device=dev)
 dgam, dbet = torch.zeros(h, device=dev), torch.zeros(h, device=dev)
 dy4 = bf(T, 4 * h)
 db4 = torch.zeros(4 * h, device=dev)
@@ -40,8 +39,6 @@ rows = [
     ("layernorm_bwd_dx (+resid)", lambda: ops.layernorm_bwd(dy, x, mean, rstd, g, dx, None, None, None, dresid=dres),
      4 * T * h * 2),
     ("norm_param_grads", lambda: ops.norm_param_grads(dy, x, mean, rstd, dgam, dbet, ws), 2 * T * h * 2),
-    ("norm_bwd_fused (dx+dg+db)", lambda: ops.norm_bwd_fused(dy, x, mean, rstd, g, dx, dgam, dbet, part, dresid=dres),
-     4 * T * h * 2),
     ("colsum (bias grad, 4h)", lambda: ops.colsum_acc(dy4, db4, ws), T * 4 * h * 2),
     ("adamw (256 M params)", lambda: ops.adamw(pm, m, v, gr, pb, 1e-4, 0.9, 0.95, 1e-8, 0.1, 1), n_opt * 30),
 ]
