@@ -188,14 +188,18 @@ class Runtime:
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
                  aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True,
-                 rs_wire: str = "bf16", stream_priority: bool = False):
+                 rs_wire: str = "bf16", stream_priority: bool = False, nccl_max_channels: int | None = 8):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
         (first two steps, debugging); ``memory_check``: refuse configurations whose estimated
-        peak does not fit (see below); ``rs_wire``: "bf16" (the reference's byte model,
+        peak does not fit (see below); ``nccl_max_channels``: cap on the CTAs (channels) an NCCL
+        collective may occupy -- NCCL's default takes SMs the concurrent GEMMs need (N=4 P2 x D2:
+        8 channels +4.0% tokens/s vs the default, profiles/r02/nccl_channels_ab.txt; None keeps
+        NCCL's choice; an NCCL_MAX_NCHANNELS already in the environment wins); ``rs_wire``: "bf16" (the reference's byte model,
         `schedules.py:76-78`) or "fp32" (RS_GRAD sums in fp32 on the wire: twice the bytes, no
         bf16 rounding of the partial sums -- tools/rs_wire_drift.py measures the difference)."""
+        self.nccl_max_channels = nccl_max_channels
         if rs_wire not in ("bf16", "fp32"):
             raise ValueError("rs_wire must be 'bf16' or 'fp32'")
         self.rs_wire = rs_wire
@@ -301,6 +305,8 @@ class Runtime:
         Keys are node-local; a rank only joins the communicators of its own node, plus
         ("inter",) = its (p, z) peers in the other n - 1 replicas."""
         import torch.distributed as dist
+        if self.nccl_max_channels:
+            os.environ.setdefault("NCCL_MAX_NCHANNELS", str(self.nccl_max_channels))  # read at NCCL init
         lib.load_nccl()
         plan = comm_plan(self.n, self.P, self.D)
         import ctypes
