@@ -210,8 +210,10 @@ def run_zpp(args) -> None:
     barrier()
     ev0.record(comp)
     results = []
+    t_host = time.perf_counter()
     for k in range(args.steps):
         results.append(rt.step(ids_ds[k % NB], lab_ds[k % NB]))
+    host_ms = (time.perf_counter() - t_host) * 1e3  # enqueue time: the host runs ahead of the GPU
     ev1.record(comp)
     barrier()
     launches = ops.PROFILE.launches
@@ -278,6 +280,7 @@ def run_zpp(args) -> None:
             "mfu": {"vs_2250_dense": round(value * flops_tok / (N * PEAK_DENSE_TF * 1e12), 4),
                     f"vs_{kind}_{sustained}": round(value * flops_tok / (N * sustained * 1e12), 4)},
             "exposed_comm_ms_per_step": round(exposed_ms, 3),
+            "host_enqueue_ms_per_step": round(host_ms / args.steps, 1),
             "p2p_wait_ms_per_step": round(p2p_ms, 3),
             "loss": round(loss, 5),
             "max_mem_gb": round(mem_gb, 1),
