@@ -8,7 +8,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2402_03791_b200.engine import ops  # noqa: E402
+from paper_2402_03791_b200.engine import lib, ops  # noqa: E402
+
+if os.environ.get("ZPP_LIB_AB"):  # A/B against another build of the library (tools only)
+    lib.LIB_PATH = os.environ["ZPP_LIB_AB"]
 
 b, s, H, D = 2, 2048, 32, 128
 if len(sys.argv) > 1:
