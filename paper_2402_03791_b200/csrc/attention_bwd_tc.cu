@@ -56,12 +56,6 @@ __device__ unsigned long long g_attn_trace[2][8][64];
 
 namespace {
 constexpr float kLog2e = 1.4426950408889634f;
-// dK / dV row warps: which of each thread's 16 exponentials per tile run on the FMA pipe
-// (exp2_fma) rather than the MUFU unit, whose queue otherwise stalls the exp phase
-#ifndef ZPP_EXP_FMA_MASK
-#define ZPP_EXP_FMA_MASK 0x5050
-#endif
-constexpr unsigned kExpFmaMask = ZPP_EXP_FMA_MASK;
 
 __device__ __forceinline__ float dot8(uint4 a, uint4 b) {
   float s = bf16lo(a.x) * bf16lo(b.x);
@@ -93,7 +87,7 @@ __device__ __forceinline__ void warp_arrive(uint32_t bar) {
 // one thread can then TMA-store the whole tile: each warp writing 32 different rows straight
 // to global memory cost ~4k cycles of uncoalesced stores per tile (measured, dK/dV epilogue).
 template <int W>
-__device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int c0, uint32_t tile, float mul = 1.f) {
+__device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int c0, uint32_t tile) {
   uint32_t v[32];
   if constexpr (W == 32) {
     tmem_ld32(tacc + lo + c0, v);
@@ -106,10 +100,10 @@ __device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int
     const int col = c0 + k;  // multiple of 8: one 16-byte chunk
     const uint32_t atom = tile + (col >> 6) * (128 * 128), chunk = (col & 63) >> 3;
     st_shared_v4(atom + r * 128 + ((chunk ^ (r & 7)) << 4),
-                 pack_bf16(__uint_as_float(v[k]) * mul, __uint_as_float(v[k + 1]) * mul),
-                 pack_bf16(__uint_as_float(v[k + 2]) * mul, __uint_as_float(v[k + 3]) * mul),
-                 pack_bf16(__uint_as_float(v[k + 4]) * mul, __uint_as_float(v[k + 5]) * mul),
-                 pack_bf16(__uint_as_float(v[k + 6]) * mul, __uint_as_float(v[k + 7]) * mul));
+                 pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                 pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
+                 pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
+                 pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
   }
 }
 
@@ -736,9 +730,8 @@ __global__ void __launch_bounds__(768, 1)
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float x = fmaf(__uint_as_float(sv[jj + u]), sl2, -lv[u]);
-            p[jj + u] = (kExpFmaMask >> (jj + u)) & 1 ? exp2_fma(x) : fast_exp2(x);
-            ds[jj + u] = dv[u];
+            p[jj + u] = fast_exp2(fmaf(__uint_as_float(sv[jj + u]), sl2, -lv[u]));
+            ds[jj + u] = dv[u] * scale;
           }
         }
         if (it < 2) {  // tiles on the diagonal: key after query
@@ -748,7 +741,7 @@ __global__ void __launch_bounds__(768, 1)
             if (qk + jj < 0) p[jj] = 0.f;
         }
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) ds[jj] = p[jj] * (__uint_as_float(pv[jj]) - ds[jj]);  // dS / scale
+        for (int jj = 0; jj < 16; ++jj) ds[jj] = p[jj] * fmaf(__uint_as_float(pv[jj]), scale, -ds[jj]);
         if (threadIdx.x == 128 && j < 8) ZTRACE(1, 6, it);
         if (g >= 1) mbar_wait(ds_free, (g - 1) & 1);  // dV / dK of the previous tile done reading P^T / dS^T
         const uint32_t rp = base + C::PT_OFF + r * 128, rd = base + C::DS_OFF + r * 128;
@@ -789,7 +782,7 @@ __global__ void __launch_bounds__(768, 1)
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < D; c += 32) {
-        stage_acc<32>(T_DK, lo, r, c, base + C::K_OFF, scale);  // dK = scale * sum (dS / scale)^T Q
+        stage_acc<32>(T_DK, lo, r, c, base + C::K_OFF);
         stage_acc<32>(T_DV, lo, r, c, base + C::V_OFF);
       }
       tc_fence_before();
@@ -815,345 +808,6 @@ __global__ void __launch_bounds__(768, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-// ---------------------------------------------------------------------------------------
-// dK / dV on CTA pairs (d = 128, T % 256 == 0).  The single-CTA kernel above is bound by
-// shared-memory bandwidth, not by the tensor core: per 64-query tile ~160 KB pass through smem
-// (TMA writes, P^T / dS^T writes, and the MMAs re-reading the full Q / dO B operands of all
-// four products) against ~1024 tensor-core cycles of math.  Here a 2-CTA cluster owns 256
-// keys: CTA `rank` holds keys [128 rank, 128 rank + 128) of the pair in its TMEM lanes and
-// smem, and the leader's MMA warp issues every product as one cta_group::2 MMA (M = 256), for
-// which each CTA supplies HALF of the B operand - 32 of the 64 query rows for S^T / dP^T, 64 of
-// the d columns for dV / dK - 128 KB of smem traffic per CTA and tile.
-// Roles, pipeline and TMEM layout as in the single-CTA kernel; the row warps and epilogue warps
-// of both CTAs arrive on the leader's kv_tmem / sp_free / ds_full / acc_free, the leader's
-// commits reach the same barrier offset in both CTAs, each CTA's TMA bytes complete the leader's
-// qd_full.  Items are (256-key pair block, head), walked in snake order per cluster.  The pair's
-// second CTA computes two fully masked query tiles per item (its keys start 128 later): ~3%.
-struct BwdDkdv2Cfg {
-  static constexpr int D = 128;
-  static constexpr int KATOM = 128 * 128;  // [128 rows][64 bf16]
-  static constexpr int KTILE = (D / 64) * KATOM;
-  static constexpr int RATOM = 32 * 128;   // [32 query rows][64 bf16]: this CTA's half of S^T's B
-  static constexpr int CATOM = 64 * 128;   // [64 query rows][64 d cols]: this CTA's half of dK's B
-  static constexpr int QR = 0, DR = QR + (D / 64) * RATOM, QC = DR + (D / 64) * RATOM, DC = QC + CATOM;
-  static constexpr int STAGE = DC + CATOM;  // 32 KB: Q, dO rows-half + Q, dO cols-half
-  static constexpr int QST = 3;
-  static constexpr int PT_BYTES = 128 * 128;  // P^T or dS^T: [128 keys][64 queries] bf16
-  static constexpr int K_OFF = 0;
-  static constexpr int V_OFF = K_OFF + KTILE;
-  static constexpr int S_OFF = V_OFF + KTILE;
-  static constexpr int PT_OFF = S_OFF + QST * STAGE;  // [2] P^T, double-buffered
-  static constexpr int DS_OFF = PT_OFF + 2 * PT_BYTES;  // [2] dS^T
-  static constexpr int L_OFF = DS_OFF + 2 * PT_BYTES;  // per stage: lse2 [64] | delta [64]
-  static constexpr int BAR_OFF = L_OFF + QST * 512;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr int THREADS = 768;
-  static_assert(SMEM <= 232448, "smem budget");
-};
-
-__device__ __forceinline__ void warp_arrive_remote(uint32_t cluster_bar) {
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive_remote(cluster_bar);
-}
-
-__global__ void __launch_bounds__(768, 1)
-    attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q32,
-                          const __grid_constant__ CUtensorMap tm_do32, const __grid_constant__ CUtensorMap tm_q64,
-                          const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_st,
-                          const float* __restrict__ lse2, const float* __restrict__ delta, int T, int H, int BH,
-                          float scale) {
-  using C = BwdDkdv2Cfg;
-  constexpr int D = C::D, NA = D / 64;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t bars = base + C::BAR_OFF;
-  const uint32_t kv_full = bars, qd_full0 = bars + 8, qd_empty0 = qd_full0 + 8 * C::QST;
-  const uint32_t l_full0 = qd_empty0 + 8 * C::QST, kv_tmem = l_full0 + 8 * C::QST, kv_loc = kv_tmem + 8;
-  const uint32_t sp_full = kv_loc + 8, sp_free = sp_full + 8, ds_full0 = sp_free + 8, ds_free0 = ds_full0 + 16;
-  const uint32_t mm_done = ds_free0 + 16, acc_free = mm_done + 8, kv_empty = acc_free + 8;
-  static_assert(8 * (3 * C::QST + 12) <= 240, "barrier area");
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = static_cast<int>(cluster_rank());
-  const bool leader = rank == 0;
-  const int cid = blockIdx.x >> 1, G = gridDim.x >> 1;
-  const int nitems = (T / 256) * BH;
-  auto decode = [&](int w, int& bh, int& k0, int& nq) {  // item w -> (head, first key of the pair, tiles)
-    bh = w % BH;
-    const int kp = w / BH;
-    k0 = kp * 256;
-    nq = 4 * (T / 256 - kp);
-  };
-
-  if (threadIdx.x == 0) {
-    tma_prefetch(&tm_kv);
-    tma_prefetch(&tm_q32);
-    tma_prefetch(&tm_do32);
-    tma_prefetch(&tm_q64);
-    tma_prefetch(&tm_do64);
-    tma_prefetch(&tm_st);
-    mbar_init(kv_full, 1);
-    for (int s = 0; s < C::QST; ++s) {
-      mbar_init(qd_full0 + 8 * s, 1);  // the leader's expect_tx; both CTAs' bytes
-      mbar_init(qd_empty0 + 8 * s, 1);
-      mbar_init(l_full0 + 8 * s, 1);
-    }
-    mbar_init(kv_tmem, 32);  // row warps of both CTAs (used in the leader)
-    mbar_init(kv_loc, 16);   // this CTA's row warps
-    mbar_init(sp_full, 1);
-    mbar_init(sp_free, 32);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(ds_full0 + 8 * s, 32);
-      mbar_init(ds_free0 + 8 * s, 1);
-    }
-    mbar_init(mm_done, 1);
-    mbar_init(acc_free, 8);  // epilogue warps of both CTAs
-    mbar_init(kv_empty, 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc2(smem_u32(tmem_slot), 512);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t T_DV = tmem, T_DK = tmem + D, T_K = tmem + 2 * D, T_V = T_K + D / 2, T_S = tmem + 3 * D,
-                 T_DP = T_S + 64;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int g = 0;
-      for (int k = 0, jn = 0; k * G < nitems; ++k) {
-        const int w = snake_item(k, G, cid);
-        if (w >= nitems) continue;
-        const int j = jn++;
-        int bh, k0, nq;
-        decode(w, bh, k0, nq);
-        const int b = bh / H, h = bh % H, row_base = b * T;
-        if (j == 1) mbar_wait(kv_loc, 0);
-        if (j >= 2) mbar_wait(kv_empty, (j - 2) & 1);
-        mbar_arrive_expect_tx(kv_full, 2 * C::KTILE);
-        for (int a = 0; a < NA; ++a) {
-          tma_load_2d(base + C::K_OFF + a * C::KATOM, &tm_kv, kv_full, H * D + h * D + 64 * a,
-                      row_base + k0 + 128 * rank);
-          tma_load_2d(base + C::V_OFF + a * C::KATOM, &tm_kv, kv_full, 2 * H * D + h * D + 64 * a,
-                      row_base + k0 + 128 * rank);
-        }
-        for (int it = 0; it < nq; ++it, ++g) {
-          const int st = g % C::QST;
-          const int q0 = k0 + it * 64;
-          mbar_wait(qd_empty0 + 8 * st, ((g / C::QST) & 1) ^ 1);
-          const uint32_t fb = qd_full0 + 8 * st, sb = base + C::S_OFF + st * C::STAGE;
-          if (leader) mbar_arrive_expect_tx(fb, 2 * C::STAGE);
-          for (int a = 0; a < NA; ++a) {
-            tma_load_2d_2sm(sb + C::QR + a * C::RATOM, &tm_q32, fb, h * D + 64 * a, row_base + q0 + 32 * rank);
-            tma_load_2d_2sm(sb + C::DR + a * C::RATOM, &tm_do32, fb, h * D + 64 * a, row_base + q0 + 32 * rank);
-          }
-          tma_load_2d_2sm(sb + C::QC, &tm_q64, fb, h * D + 64 * rank, row_base + q0);
-          tma_load_2d_2sm(sb + C::DC, &tm_do64, fb, h * D + 64 * rank, row_base + q0);
-          if (g == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // delta / lse2 of the dQ kernel
-          const uint32_t lb = l_full0 + 8 * st;
-          mbar_arrive_expect_tx(lb, 512);
-          bulk_load_1d(base + C::L_OFF + st * 512, lse2 + (long long)bh * T + q0, 256, lb);
-          bulk_load_1d(base + C::L_OFF + st * 512 + 256, delta + (long long)bh * T + q0, 256, lb);
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (leader) {  // whole warp: uniform descriptors, elect.sync issues
-      constexpr uint32_t id_sp = make_idesc_bf16(256, 64, false, false);  // S^T, dP^T: M = 256 keys, N = 64
-      constexpr uint32_t id_kv = make_idesc_bf16(256, D, false, true);    // dV, dK: B N-major (N = d)
-      auto issue_sp = [&](int g) {
-        const int st = g % C::QST;
-        mbar_wait(qd_full0 + 8 * st, (g / C::QST) & 1);
-        tc_fence_after();
-        const uint32_t sb = base + C::S_OFF + st * C::STAGE;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_ts_2sm_w(T_S, T_K + kk * 8, make_sdesc(sb + C::QR + (kk >> 2) * C::RATOM + (kk & 3) * 32, 16, 1024),
-                            id_sp, kk > 0 ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_ts_2sm_w(T_DP, T_V + kk * 8, make_sdesc(sb + C::DR + (kk >> 2) * C::RATOM + (kk & 3) * 32, 16, 1024),
-                            id_sp, kk > 0 ? 1u : 0u);
-        mma_commit_2sm_w(sp_full);
-      };
-      int g = 0;
-      for (int k = 0, jn = 0; k * G < nitems; ++k) {
-        const int w = snake_item(k, G, cid);
-        if (w >= nitems) continue;
-        const int j = jn++;
-        int bh, k0, nq;
-        decode(w, bh, k0, nq);
-        mbar_wait(kv_tmem, j & 1);  // K, V(j) in both CTAs' TMEM; S^T / dP^T of item j-1 loaded
-        tc_fence_after();
-        issue_sp(g);
-        for (int it = 0; it < nq; ++it, ++g) {
-          const int st = g % C::QST;
-          const uint32_t sb = base + C::S_OFF + st * C::STAGE;
-          if (it + 1 < nq) {
-            mbar_wait(sp_free, g & 1);
-            tc_fence_after();
-            issue_sp(g + 1);
-          }
-          const int pb = g & 1;  // P^T / dS^T buffer of tile g
-          mbar_wait(ds_full0 + 8 * pb, (g >> 1) & 1);
-          tc_fence_after();
-          if (it == 0 && j > 0) {
-            mbar_wait(acc_free, (j - 1) & 1);
-            tc_fence_after();
-          }
-          const uint32_t acc0 = it > 0 ? 1u : 0u;
-          const uint32_t pts = base + C::PT_OFF + pb * C::PT_BYTES, dss = base + C::DS_OFF + pb * C::PT_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO
-            mma_bf16_2sm_w(T_DV, make_sdesc(pts + kk * 32, 16, 1024), make_sdesc(sb + C::DC + kk * 2048, C::CATOM, 1024),
-                           id_kv, (acc0 | kk) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q
-            mma_bf16_2sm_w(T_DK, make_sdesc(dss + kk * 32, 16, 1024), make_sdesc(sb + C::QC + kk * 2048, C::CATOM, 1024),
-                           id_kv, (acc0 | kk) ? 1u : 0u);
-          mma_commit_2sm_w(ds_free0 + 8 * pb);
-          mma_commit_2sm_w(qd_empty0 + 8 * st);
-        }
-        mma_commit_2sm_w(mm_done);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4 && warp < 20) {
-    const int q = warp & 3;
-    const int part = (warp - 4) >> 2;
-    const int r = q * 32 + lane;       // key row within this CTA == TMEM lane
-    const int rk = r + 128 * rank;     // key row within the pair
-    const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
-    const float sl2 = scale * kLog2e;
-    const uint32_t kv_tmem_l = map_cta(kv_tmem, 0), sp_free_l = map_cta(sp_free, 0),
-                   ds_full_l = map_cta(ds_full0, 0);
-    int g = 0;
-    for (int k = 0, jn = 0; k * G < nitems; ++k) {
-      const int w = snake_item(k, G, cid);
-      if (w >= nitems) continue;
-      const int j = jn++;
-      int bh, k0, nq;
-      decode(w, bh, k0, nq);
-      {  // K and V rows of item j -> TMEM (key row r, quarter `part` of the D columns)
-        constexpr int CH = D / 32;
-        uint32_t kv[4 * CH], vv[4 * CH];
-        mbar_wait(kv_full, j & 1);
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          const int cg = part * CH + i;
-          const uint32_t off = (cg >> 3) * C::KATOM + r * 128 + (((cg & 7) ^ (r & 7)) << 4);
-          const uint4 k4 = ld_shared_v4(base + C::K_OFF + off), v4 = ld_shared_v4(base + C::V_OFF + off);
-          kv[4 * i] = k4.x, kv[4 * i + 1] = k4.y, kv[4 * i + 2] = k4.z, kv[4 * i + 3] = k4.w;
-          vv[4 * i] = v4.x, vv[4 * i + 1] = v4.y, vv[4 * i + 2] = v4.z, vv[4 * i + 3] = v4.w;
-        }
-        tmem_st16(T_K + lo + part * 16, kv);
-        tmem_st16(T_V + lo + part * 16, vv);
-        tmem_wait_st();
-        tc_fence_before();
-        warp_arrive(kv_loc);
-        warp_arrive_remote(kv_tmem_l);
-      }
-      for (int it = 0; it < nq; ++it, ++g) {
-        const int st = g % C::QST;
-        const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + st * 512) + part * 16;
-        mbar_wait(sp_full, g & 1);
-        tc_fence_after();
-        uint32_t sv[16], pv[16];
-        tmem_ld16(T_S + lo + part * 16, sv);
-        tmem_ld16(T_DP + lo + part * 16, pv);
-        tmem_wait_ld();
-        tc_fence_before();
-        warp_arrive_remote(sp_free_l);
-        mbar_wait(l_full0 + 8 * st, (g / C::QST) & 1);
-        float p[16], ds[16];
-#pragma unroll
-        for (int jj = 0; jj < 16; jj += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(L + jj);
-          const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + jj);
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float x = fmaf(__uint_as_float(sv[jj + u]), sl2, -lv[u]);
-            p[jj + u] = (kExpFmaMask >> (jj + u)) & 1 ? exp2_fma(x) : fast_exp2(x);
-            ds[jj + u] = dv[u];
-          }
-        }
-        if (it < 2 + 2 * rank) {  // tiles on (or, for the second CTA, before) the diagonal
-          const int qk = it * 64 + part * 16 - rk;
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
-            if (qk + jj < 0) p[jj] = 0.f;
-        }
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) ds[jj] = p[jj] * (__uint_as_float(pv[jj]) - ds[jj]);  // dS / scale
-        const int pb = g & 1;  // buffer pb was last read by dV / dK of tile g-2
-        if (g >= 2) mbar_wait(ds_free0 + 8 * pb, ((g >> 1) & 1) ^ 1);
-        const uint32_t rp = base + C::PT_OFF + pb * C::PT_BYTES + r * 128,
-                       rd = base + C::DS_OFF + pb * C::PT_BYTES + r * 128;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int c8 = part * 2 + t;
-          const float* pp = &p[t * 8];
-          const float* sd = &ds[t * 8];
-          const uint32_t sw = (c8 ^ (r & 7)) << 4;
-          st_shared_v4(rp + sw, pack_bf16(pp[0], pp[1]), pack_bf16(pp[2], pp[3]), pack_bf16(pp[4], pp[5]),
-                       pack_bf16(pp[6], pp[7]));
-          st_shared_v4(rd + sw, pack_bf16(sd[0], sd[1]), pack_bf16(sd[2], sd[3]), pack_bf16(sd[4], sd[5]),
-                       pack_bf16(sd[6], sd[7]));
-        }
-        fence_proxy_async();
-        warp_arrive_remote(ds_full_l + 8 * pb);
-      }
-    }
-  } else if (warp >= 20) {
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t acc_free_l = map_cta(acc_free, 0);
-    for (int k = 0, jn = 0; k * G < nitems; ++k) {
-      const int w = snake_item(k, G, cid);
-      if (w >= nitems) continue;
-      const int j = jn++;
-      int bh, k0, nq;
-      decode(w, bh, k0, nq);
-      const int b = bh / H, h = bh % H, row_base = b * T;
-      bool more = false;
-      for (int k2 = k + 1; k2 * G < nitems && !more; ++k2) more = snake_item(k2, G, cid) < nitems;
-      mbar_wait(mm_done, j & 1);
-      if (more) mbar_wait(kv_loc, (j + 1) & 1);  // staging area = K / V smem, free once K / V(j+1) sit in TMEM
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < D; c += 32) {
-        stage_acc<32>(T_DK, lo, r, c, base + C::K_OFF, scale);  // dK = scale * sum (dS / scale)^T Q
-        stage_acc<32>(T_DV, lo, r, c, base + C::V_OFF);
-      }
-      tc_fence_before();
-      warp_arrive_remote(acc_free_l);
-      fence_proxy_async();
-      named_bar_sync(2, 128);
-      if (threadIdx.x == 640) {
-        for (int a = 0; a < NA; ++a) {
-          tma_store_2d(&tm_st, base + C::K_OFF + a * C::KATOM, H * D + h * D + 64 * a, row_base + k0 + 128 * rank);
-          tma_store_2d(&tm_st, base + C::V_OFF + a * C::KATOM, 2 * H * D + h * D + 64 * a,
-                       row_base + k0 + 128 * rank);
-        }
-        bulk_commit();
-        bulk_wait_all();
-        mbar_arrive(kv_empty);
-      }
-    }
-  }
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc2(tmem, 512);
-}
-
 namespace {
 int qkv_map(CUtensorMap* m, const void* p, int H, int D, int cols_mult, int rows_total, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)cols_mult * H * D, (cuuint64_t)rows_total};
@@ -1171,8 +825,6 @@ cudaError_t bwd_attrs() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              BwdDkdvCfg<D>::SMEM);
-  if (e == cudaSuccess && D == 128)
-    e = cudaFuncSetAttribute(attn_bwd_dkdv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdDkdv2Cfg::SMEM);
   return e;
 }
 }  // namespace
@@ -1210,41 +862,18 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
   if (rc) return rc;
   // dK/dV launched as a programmatic dependent of the dQ kernel: its prologue (TMEM, barriers,
   // K/V/Q/dO loads) runs on SMs the dQ tail leaves idle; only the lse2 / delta loads wait
-#ifndef ZPP_DKDV_PAIR
-#define ZPP_DKDV_PAIR 1
-#endif
-  const bool pair = ZPP_DKDV_PAIR && D == 128 && T % 256 == 0;
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[2];
+  cfg.gridDim = pgrid;
+  cfg.blockDim = dim3(BwdDkdvCfg<D>::THREADS);
+  cfg.dynamicSmemBytes = BwdDkdvCfg<D>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = 2;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.stream = s;
-  cudaError_t e;
-  if (pair) {
-    CUtensorMap m_q32, m_do32;
-    rc = qkv_map(&m_q32, qkv, H, D, 3, BT, 32);
-    if (!rc) rc = qkv_map(&m_do32, dout, H, D, 1, BT, 32);
-    if (rc) return rc;
-    const int pitems = (T / 256) * BH, pairs = num_sms() / 2;
-    cfg.gridDim = dim3(2 * (pitems < pairs ? pitems : pairs));
-    cfg.blockDim = dim3(BwdDkdv2Cfg::THREADS);
-    cfg.dynamicSmemBytes = BwdDkdv2Cfg::SMEM;
-    cfg.numAttrs = 2;
-    e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv2_kernel, m_kv128, m_q32, m_do32, m_q64, m_do64, m_st,
-                           (const float*)lse2, (const float*)delta, T, H, BH, scale);
-  } else {
-    cfg.gridDim = pgrid;
-    cfg.blockDim = dim3(BwdDkdvCfg<D>::THREADS);
-    cfg.dynamicSmemBytes = BwdDkdvCfg<D>::SMEM;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, m_st, (const float*)lse2,
-                           (const float*)delta, T, H, BH, scale);
-  }
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, m_st, (const float*)lse2,
+                                     (const float*)delta, T, H, BH, scale);
   if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv launch");
   return check_launch("attn_bwd_dkdv");
 }

@@ -251,17 +251,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x for x <= ~0 on the FMA / ALU pipes instead of the MUFU unit (16 ex2 / clk / SM), to
-// split an exp-heavy phase across both: x = n + f with n = rint(x) by the 1.5*2^23 shift,
-// degree-3 relative-minimax 2^f on [-1/2, 1/2] (max rel. error 7.5e-5, far below the bf16
-// rounding of the result), n added into the exponent field.  x is clamped at -125: 2^-125 ~ 0.
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.055170949548f, f, 0.242609634995f), f, 0.693260967731f), f, 0.999928176403f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 }  // namespace zpp
 
 namespace zpp {
@@ -354,32 +343,6 @@ __device__ __forceinline__ void mma_commit_w(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-      : "memory");
-}
-// CTA-pair (cta_group::2) forms of the warp-collective issue above, for the leader CTA.
-__device__ __forceinline__ void mma_bf16_2sm_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_bf16_ts_2sm_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                                  uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Commit to the barrier at this smem offset in both CTAs of the pair.
-__device__ __forceinline__ void mma_commit_2sm_w(uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          bar),
-      "h"((uint16_t)0x3)
       : "memory");
 }
 }  // namespace zpp
