@@ -19,13 +19,16 @@ ap.add_argument("--U", type=int, default=2)
 ap.add_argument("--mb", type=int, default=2, help="samples per micro-batch (bench default b=2)")
 ap.add_argument("--ncu", action="store_true")
 ap.add_argument("--gemm-shapes", default=None, help="with --ncu: write M,N,K,algorithmic bytes per GEMM launch")
+ap.add_argument("--rt", default="", help="Runtime keyword overrides, e.g. 'aux_stream=False'")
 a = ap.parse_args()
+import ast
+rt_kw = {k: ast.literal_eval(v) for k, v in (kv.split("=") for kv in a.rt.split(",") if kv)}
 spec = GPTSpec(num_layers=a.layers, hidden=4096, heads=32, seq_len=2048, microbatch_samples=a.mb)
 model = ModelSpec(num_layers=spec.num_layers, hidden_size=spec.hidden, seq_len=spec.seq_len)
 cfg = ParallelConfig(pp_size=1, dp_size=1, microbatches=a.B, unit_size=a.U, microbatch_samples=a.mb)
 pl = make_placement(cfg, model)
 sched = generate(model, cfg, pl)
-rt = Runtime(spec, model, cfg, pl, sched)
+rt = Runtime(spec, model, cfg, pl, sched, **rt_kw)
 t = make_tokens(1, 1, a.B, a.mb, spec.seq_len, spec.vocab)[0, 0]
 ids = t[:, :, :-1].reshape(a.B, -1).contiguous().cuda()
 lab = t[:, :, 1:].reshape(a.B, -1).contiguous().cuda()
