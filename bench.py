@@ -172,7 +172,9 @@ def run_zpp(args) -> None:
                          microbatch_samples=mbs)
     pl = make_placement(cfg, model)
     sched = generate(model, cfg, pl)
-    rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=True)
+    import ast
+    rt_kw = {k: ast.literal_eval(v) for k, v in (kv.split("=") for kv in args.rt.split(",") if kv)}
+    rt = Runtime(spec, model, cfg, pl, sched, rank=rank, world=world, timeline=True, **rt_kw)
     z = rt.z
     # NB distinct synthetic batches, cycled step by step: a repeated batch would be memorised
     # within a few steps (loss -> 0), which is not a training workload
@@ -214,6 +216,7 @@ def run_zpp(args) -> None:
     for k in range(args.steps):
         results.append(rt.step(ids_ds[k % NB], lab_ds[k % NB]))
     host_ms = (time.perf_counter() - t_host) * 1e3  # enqueue time: the host runs ahead of the GPU
+    rt.join(comp)  # the last step's tail (reduce-scatters / AdamW on side streams) is inside the region
     ev1.record(comp)
     barrier()
     launches = ops.PROFILE.launches
@@ -243,6 +246,7 @@ def run_zpp(args) -> None:
 
     # ---- end-to-end through the public API (host buffers in the timed region) --
     barrier()
+    timeline, rt.timeline = rt.timeline, False  # no per-task events: execute() syncs only on the step's end
     t_e2e = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -252,8 +256,10 @@ def run_zpp(args) -> None:
         lab_d.copy_(lab_hs[k % NB], non_blocking=True)
         r = execute(sched, model, cfg, pl, rt, ids_d, lab_d)
         _ = r.loss_sum.item()
+    rt.join()
     e1.record()
     barrier()
+    rt.timeline = timeline
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t_e2e) * 1e3))
     mem_gb = max_over_ranks(torch.cuda.max_memory_allocated() / 1e9)
 
@@ -276,6 +282,8 @@ def run_zpp(args) -> None:
                        "global_batch": D * B * mbs, "seq_len": spec.seq_len, "parallelism": f"pp{P}xzero{D}",
                        "tokens_per_step": tokens_per_step,
                        "cuda_graph": rt._graph is not None,
+                       "overlap_tail": rt._tail_overlaps(),
+                       **({"runtime_overrides": args.rt} if args.rt else {}),
                        "l2": "inputs larger than L2 (each step streams >10 GB of weights/activations)"},
             "mfu": {"vs_2250_dense": round(value * flops_tok / (N * PEAK_DENSE_TF * 1e12), 4),
                     f"vs_{kind}_{sustained}": round(value * flops_tok / (N * sustained * 1e12), 4)},
@@ -455,6 +463,7 @@ def main() -> None:
     ap.add_argument("--mb-size", type=int, default=None,
                     help="samples per micro-batch (ParallelConfig.microbatch_samples); default from the split")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out"))
+    ap.add_argument("--rt", default="", help="Runtime keyword overrides for A/B runs, e.g. 'overlap_tail=False'")
     args = ap.parse_args()
     os.makedirs(args.out_dir, exist_ok=True)
     if args.warmup < 3 and args.impl == "zpp":

@@ -188,7 +188,8 @@ class Runtime:
                  sched: Schedule, rank: int = 0, world: int = 1, device: int | None = None,
                  timeline: bool = False, early_opt: bool | None = None, cuda_graph: bool = False,
                  aux_stream: bool = True, host_trace: bool = False, memory_check: bool = True,
-                 rs_wire: str = "bf16", stream_priority: bool = False, nccl_max_channels: int | None = 8):
+                 rs_wire: str = "bf16", stream_priority: bool = False, nccl_max_channels: int | None = 8,
+                 overlap_tail: bool = True):
         """``early_opt``: None = auto (on when D > 1, see below); ``cuda_graph``: replay the
         task list as a CUDA graph (one rank); ``aux_stream``: bias / norm-parameter column
         reductions on a side stream; ``host_trace``: print each task as it is enqueued
@@ -198,7 +199,10 @@ class Runtime:
         8 channels +4.0% tokens/s vs the default, profiles/r02/nccl_channels_ab.txt; None keeps
         NCCL's choice; an NCCL_MAX_NCHANNELS already in the environment wins); ``rs_wire``: "bf16" (the reference's byte model,
         `schedules.py:76-78`) or "fp32" (RS_GRAD sums in fp32 on the wire: twice the bytes, no
-        bf16 rounding of the partial sums -- tools/rs_wire_drift.py measures the difference)."""
+        bf16 rounding of the partial sums -- tools/rs_wire_drift.py measures the difference);
+        ``overlap_tail``: with the early optimizer, the step's last reduce-scatters and AdamW
+        run on their side streams into the next step's first forward tasks instead of holding
+        the compute stream at OPT (see ``_optimizer``)."""
         self.nccl_max_channels = nccl_max_channels
         if rs_wire not in ("bf16", "fp32"):
             raise ValueError("rs_wire must be 'bf16' or 'fp32'")
@@ -263,6 +267,7 @@ class Runtime:
         # at D == 1 there is nothing to overlap but the GEMMs, which under the power cap only
         # slows them (measured: profiles/r01c_ab_n1_aux_earlyopt_b2.txt), so it is off there.
         self.early_opt = self.n == 1 and (self.D > 1 if early_opt is None else bool(early_opt))
+        self.overlap_tail = bool(overlap_tail)
         self.s_opt = mk(0)
         # CUDA-graph mode (cuda_graph=True; one rank, no early optimizer): the task list up to
         # OPT is captured once, on the second step, and replayed; OPT runs eagerly after it
@@ -467,10 +472,25 @@ class Runtime:
         return StepResult(self.loss_sum, tokens_done, nccl_bytes_intra=self.nccl_bytes["intra"],
                           nccl_bytes_inter=self.nccl_bytes["inter"])
 
+    def join(self, stream=None) -> None:
+        """Order ``stream`` (default: the current stream) after all work this runtime has
+        enqueued on any of its streams -- including an overlapped step tail."""
+        stream = stream or torch.cuda.current_stream(self.dev)
+        for st in (self.s_comp, self.s_ag, self.s_rs, self.s_aux, self.s_opt, self.s_act_send, self.s_act_recv,
+                   self.s_grad_send, self.s_grad_recv):
+            if st is not stream:
+                stream.wait_stream(st)
+
     def finish_timing(self, res: StepResult) -> StepResult:
-        """Resolve CUDA-event timings of the last step (synchronizes)."""
-        torch.cuda.synchronize(self.dev)
+        """Resolve CUDA-event timings of the last step.  With a timeline this synchronizes the
+        device (every task's events); without one only the compute stream's end of step, so an
+        overlapped tail (``overlap_tail``) keeps running into the next step -- call
+        :meth:`join` or ``torch.cuda.synchronize()`` before reading parameters directly."""
         t_start, t_end, times = self._t
+        if self.timeline:
+            torch.cuda.synchronize(self.dev)
+        else:
+            t_end.synchronize()
         res.step_ms = t_start.elapsed_time(t_end)
         if self.timeline:
             res.task_times = {t: (t_start.elapsed_time(a), t_start.elapsed_time(b)) for t, (a, b) in times.items()}
@@ -536,6 +556,8 @@ class Runtime:
         self._join_aux(rs)                           # ... and their parameter-grad reductions
         self._begin(rs)
         n, ns = st.lay.numel, st.lay.shard_numel
+        if st.opt_ready is not None:
+            rs.wait_event(st.opt_ready)  # grad_shard: the previous step's AdamW read and zeroed it
         if self.rs_wire == "fp32":  # the fp32 stage grad IS the send buffer: reduce, then release it
             recv = self.rs_recv32[:ns]
             lib.call("zpp_reduce_scatter", self.comms[("rs", self.p)], st.grad_full.data_ptr(), recv.data_ptr(), ns,
@@ -621,9 +643,27 @@ class Runtime:
             self.s_opt.wait_event(ev)
         lo, hi = (0, st.nsub) if key is None else st.opt_slice(key)
         self._adamw(st, lo, hi, self.s_opt)
+        if self._tail_overlaps():
+            ops.zero(st.grad_shard, stream=self.s_opt)  # the next step's reduce-scatters accumulate here
         self._opt_ev = st.opt_ready = self._record(self.s_opt)
 
+    def _tail_overlaps(self) -> bool:
+        """Early optimizer at D > 1 (whole-stage AdamW after each stage's last RS_GRAD) with
+        every local stage covered: OPT then has nothing left to run on the compute stream."""
+        return (self.overlap_tail and self.early_opt and self.D > 1 and self.sub == 1 and not self.capture_grads
+                and not self.graph_mode and all(s in self._final_rs for s in self.stages))
+
     def _optimizer(self) -> None:
+        if self._tail_overlaps() and self._opt_done.issuperset(self.stages):
+            # Every stage's AdamW is already queued on the opt stream behind its last
+            # reduce-scatter, and zeroes its grad_shard there.  Nothing on the compute stream
+            # depends on them: the next step's AG_PARAM of a stage waits for that stage's AdamW
+            # (opt_ready), its first RS_GRAD for the zeroed grad_shard, its first W for the
+            # released grad_full (grad_free_event).  So the tail overlaps the next step's first
+            # forward tasks instead of stalling the compute stream here.  Runtime.join() orders
+            # a caller's stream after everything (bench.py's timed region ends with it).
+            self.opt_event = self._record(self.s_comp)
+            return
         for ev in self._rs_events:
             self._wait(ev, "zero")
         self._join_aux(self.s_comp)  # D == 1: bias / norm grads reduced on aux feed this update
@@ -956,7 +996,7 @@ def execute(sched: Schedule, model: ModelSpec, cfg: ParallelConfig, placement: P
             runtime: Runtime, ids: torch.Tensor, labels: torch.Tensor) -> StepResult:
     """Run one ZeroPP training step of ``sched`` on this rank (the engine's
     ``simulate``, `simulation.py:90`).  Returns a timed :class:`StepResult`; with a
-    ``timeline=True`` runtime it also carries the whole-job measured
+    ``timeline=True`` runtime (which synchronizes the device per step) it also carries the whole-job measured
     :class:`~paper_2402_03791_b200.simulation.SimResult` (``res.sim``, fields readable
     directly: ``res.makespan``, ``res.bubble_ratios``, ``res.loss`` ...) -- a
     collective over all ranks when the job is multi-rank."""

@@ -107,6 +107,7 @@ def run_engine_step(spec, P, D, B, U, V, rank=0, world=1, steps=1, timeline=True
         rt.capture_grads = k == 0
         res = execute(sched, model, cfg, pl, rt, ids, labels)
         out.append(res)
+    torch.cuda.synchronize()  # an overlapped step tail (AdamW on the opt stream) may still run
     return rt, (model, cfg, pl, sched), tokens, out
 
 

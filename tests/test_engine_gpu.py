@@ -143,7 +143,8 @@ def test_outer_dp_step_matches_oracle(tmp_path, n, P, D, B, U, V, mode):
                                        (2, 1, 8, 4, 2)])
 def test_early_optimizer_is_bit_identical(tmp_path, P, D, B, U, V):
     """3 steps with the early (chunked, overlapped) optimizer == 3 steps without it, bit for
-    bit: losses, fp32 masters and bf16 shards on every rank."""
+    bit: losses, fp32 masters and bf16 shards on every rank.  At D > 1 the early arm also runs
+    each step's tail (last RS_GRAD + AdamW) into the next step (Runtime(overlap_tail=True))."""
     world = P * D
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs (run via gpurun --gpus {world})")

@@ -42,6 +42,7 @@ for r in range(a.rounds):
         e0.record(rt.s_comp)
         for _ in range(a.steps):
             rt.step(ids, lab)
+        rt.join(rt.s_comp)
         e1.record(rt.s_comp)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
