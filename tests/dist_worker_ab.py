@@ -5,7 +5,10 @@ ZeroPP steps run twice in fresh runtimes, with the early optimizer on and off
 gradient path is deterministic (no fp32 atomics).  The reported loss is an fp32 atomic
 sum over token rows, so it is compared to 1e-6 relative.
 
-usage: torchrun --nproc-per-node P*D dist_worker_ab.py P D B U V STEPS OUTDIR
+With arm ``notail`` (8th argument) arm B keeps the early optimizer but runs each step's tail
+serially (Runtime(overlap_tail=False)) instead of overlapping it with the next step.
+
+usage: torchrun --nproc-per-node P*D dist_worker_ab.py P D B U V STEPS OUTDIR [noearly|notail]
 """
 
 import os
@@ -24,9 +27,9 @@ from engine_harness import run_engine_step  # noqa: E402
 from paper_2402_03791_b200.engine import GPTSpec  # noqa: E402
 
 
-def run(early: str, P, D, B, U, V, steps, rank, world):
+def run(early: str, P, D, B, U, V, steps, rank, world, tail: bool = True):
     rt, _, _, res = run_engine_step(GPTSpec.tiny(), P, D, B, U, V, rank=rank, world=world, steps=steps,
-                                    timeline=False, rt_kw={"early_opt": early == "1"})
+                                    timeline=False, rt_kw={"early_opt": early == "1", "overlap_tail": tail})
     assert rt.early_opt == (early == "1")
     losses = [r.loss_sum.item() for r in res]
     state = {s: (st.master.cpu(), st.shard_bf16.cpu()) for s, st in rt.stages.items()}
@@ -44,8 +47,12 @@ def main():
         dist.init_process_group("gloo")
     msg = "OK"
     try:
+        arm = sys.argv[8] if len(sys.argv) > 8 else "noearly"
         la, sa = run("1", P, D, B, U, V, steps, rank, world)
-        lb, sb = run("0", P, D, B, U, V, steps, rank, world)
+        if arm == "notail":
+            lb, sb = run("1", P, D, B, U, V, steps, rank, world, tail=False)
+        else:
+            lb, sb = run("0", P, D, B, U, V, steps, rank, world)
         fails = []
         if any(abs(a - b) > 1e-6 * abs(b) for a, b in zip(la, lb)):
             fails.append(f"losses differ: {la} vs {lb}")

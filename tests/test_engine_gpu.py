@@ -139,18 +139,21 @@ def test_outer_dp_step_matches_oracle(tmp_path, n, P, D, B, U, V, mode):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("P,D,B,U,V", [(1, 1, 4, 2, 1), (1, 1, 4, 2, 2), (2, 2, 8, 4, 2), (1, 4, 4, 2, 2),
-                                       (2, 1, 8, 4, 2)])
-def test_early_optimizer_is_bit_identical(tmp_path, P, D, B, U, V):
+@pytest.mark.parametrize("P,D,B,U,V,arm", [(1, 1, 4, 2, 1, "noearly"), (1, 1, 4, 2, 2, "noearly"),
+                                           (2, 2, 8, 4, 2, "noearly"), (1, 4, 4, 2, 2, "noearly"),
+                                           (2, 1, 8, 4, 2, "noearly"), (1, 2, 4, 2, 2, "notail"),
+                                           (2, 2, 8, 4, 2, "notail")])
+def test_early_optimizer_is_bit_identical(tmp_path, P, D, B, U, V, arm):
     """3 steps with the early (chunked, overlapped) optimizer == 3 steps without it, bit for
     bit: losses, fp32 masters and bf16 shards on every rank.  At D > 1 the early arm also runs
-    each step's tail (last RS_GRAD + AdamW) into the next step (Runtime(overlap_tail=True))."""
+    each step's tail (last RS_GRAD + AdamW) into the next step (Runtime(overlap_tail=True)); the
+    ``notail`` cases compare that against the same early optimizer with a serial tail."""
     world = P * D
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs (run via gpurun --gpus {world})")
     here = os.path.dirname(os.path.abspath(__file__))
     worker = os.path.join(here, "dist_worker_ab.py")
-    args = [str(x) for x in (P, D, B, U, V, 3)] + [str(tmp_path)]
+    args = [str(x) for x in (P, D, B, U, V, 3)] + [str(tmp_path), arm]
     if world == 1:
         cmd = [sys.executable, worker] + args
     else:
