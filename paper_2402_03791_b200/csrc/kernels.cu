@@ -262,12 +262,33 @@ __global__ void __launch_bounds__(NT) layernorm_bwd_dx_kernel(const bf16* __rest
 // Column reductions (deterministic, one launch):
 //   LN mode : out0[c] += sum_r dy[r,c] * (x[r,c]-mean[r])*rstd[r],  out1[c] += sum_r dy[r,c]
 //   SUM mode: out0[c] += sum_r dy[r,c]                               (bias gradients)
-// grid = (256-column strips, row splits).  256 threads = 32 column vectors (8 bf16) x 8 row
-// lanes, so every warp reads 512 contiguous bytes of one row.  Each block reduces its rows in
-// fixed order into a workspace slot; the last block of a strip (atomic ticket) adds the
-// split partials in split order to out.
+// grid = (256-column strips, row splits), sized to one wave.  Each block streams its row slab
+// through a 4-stage shared-memory ring of cp.async copies: bytes in flight no longer cost
+// registers -- the register-staged version kept too few loads in flight and reached 0.32 / 0.54
+// of HBM (profiles/r02/ncu_colred_summary.csv).  256 threads = 32 column vectors (8 bf16) x 8
+// row lanes; a thread copies exactly the 16-byte chunks it later reads (rows rl + 8i, vector
+// cv), so the ring needs no block barrier -- only the thread's own cp.async group waits.  Each
+// block reduces its rows in a fixed order into a workspace slot; the last block of a strip
+// (atomic ticket) adds the split partials in split order to out.
 constexpr int CR_MAX_SPLIT = 32;
 constexpr int CR_COLS = 256;
+constexpr int CR_NS = 4;  // stages
+template <bool LN>
+constexpr int colred_rps() {  // rows per stage: a 64 KB ring either way (LN streams two tensors)
+  return LN ? 16 : 32;
+}
+template <bool LN>
+constexpr int colred_smem() {
+  return CR_NS * colred_rps<LN>() * CR_COLS * 2 * (LN ? 2 : 1);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 template <bool LN>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy, long long ld,
                                                      const bf16* __restrict__ x, const float* __restrict__ mean,
@@ -276,34 +297,84 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
                                                      unsigned* __restrict__ tickets, int rows, int cols,
                                                      int ws_ld, int accumulate) {
   constexpr int NO = LN ? 2 : 1;
+  constexpr int CR_RPS = colred_rps<LN>();
+  constexpr int RPT = CR_RPS / 8;             // rows per thread and stage
+  constexpr int SLAB = CR_RPS * CR_COLS * 2;  // bytes of one tensor in one stage
+  extern __shared__ __align__(128) uint8_t cr_smem[];
   __shared__ float sh[NO][8][CR_COLS + 4];
   __shared__ unsigned last;
+  const uint32_t ring = smem_u32(cr_smem);
   const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int strip = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
   const int c0 = strip * CR_COLS + cv * 8;
+  const bool active = c0 < cols;
   const int rows_per = (rows + nsplit - 1) / nsplit;
   const int r_lo = split * rows_per, r_hi = min(rows, r_lo + rows_per);
-  float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (c0 < cols) {
-#pragma unroll 8
-    for (int r = r_lo + rl; r < r_hi; r += 8) {
-      float d[8];
-      unpack8(__ldcs(reinterpret_cast<const uint4*>(dy + (long long)r * ld + c0)), d);
-      if (LN) {
-        float xv[8];
-        unpack8(__ldcs(reinterpret_cast<const uint4*>(x + (long long)r * cols + c0)), xv);
-        const float mu = mean ? __ldg(mean + r) : 0.f, rs = __ldg(rstd + r);
+  const int nst = r_hi > r_lo ? (r_hi - r_lo + CR_RPS - 1) / CR_RPS : 0;
+  auto issue = [&](int it) {  // this thread's chunks of stage `it` into slot it % CR_NS (one group)
+    if (active && it < nst) {
+      const int s = it % CR_NS, r0 = r_lo + it * CR_RPS, nr = min(CR_RPS, r_hi - r0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          a0[j] += d[j] * (xv[j] - mu) * rs;
-          a1[j] += d[j];
+      for (int i = 0; i < RPT; ++i) {
+        const int ri = rl + 8 * i;
+        if (ri < nr) {
+          const uint32_t off = s * SLAB + ri * CR_COLS * 2 + cv * 16;
+          cp_async16(ring + off, dy + (long long)(r0 + ri) * ld + c0);
+          if (LN) cp_async16(ring + CR_NS * SLAB + off, x + (long long)(r0 + ri) * cols + c0);
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a0[j] += d[j];
       }
     }
+    cp_async_commit();  // possibly empty: keeps the group count per stage uniform
+  };
+#pragma unroll
+  for (int it = 0; it < CR_NS; ++it) issue(it);
+  float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // LN: the row statistics of a stage are loaded one stage ahead (their L2 latency would
+  // otherwise sit on every stage's critical path)
+  float mu_n[RPT], rs_n[RPT];
+  auto stats = [&](int it) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = min(r_lo + it * CR_RPS + rl + 8 * i, rows - 1);
+      mu_n[i] = (LN && mean) ? __ldg(mean + r) : 0.f;
+      rs_n[i] = LN ? __ldg(rstd + r) : 0.f;
+    }
+  };
+  if (LN) stats(0);
+  for (int it = 0; it < nst; ++it) {
+    const int s = it % CR_NS, r0 = r_lo + it * CR_RPS, nr = min(CR_RPS, r_hi - r0);
+    float mu_c[RPT], rs_c[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) mu_c[i] = mu_n[i], rs_c[i] = rs_n[i];
+    if (LN && it + 1 < nst) stats(it + 1);
+    cp_async_wait<CR_NS - 1>();  // stage it's group (groups complete in order)
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int ri = rl + 8 * i;
+        if (ri < nr) {
+          const uint32_t off = s * SLAB + ri * CR_COLS * 2 + cv * 16;
+          float d[8];
+          unpack8(ld_shared_v4(ring + off), d);
+          if (LN) {
+            float xv[8];
+            unpack8(ld_shared_v4(ring + CR_NS * SLAB + off), xv);
+            const float mu = mu_c[i], rs = rs_c[i];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              a0[j] += d[j] * (xv[j] - mu) * rs;
+              a1[j] += d[j];
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a0[j] += d[j];
+          }
+        }
+      }
+    }
+    issue(it + CR_NS);  // the slot this thread just read (its own chunks only)
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     sh[0][rl][cv * 8 + j] = a0[j];
@@ -343,11 +414,15 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ dy
   if (threadIdx.x == 0) tickets[strip] = 0;  // re-arm for the next launch (stream-ordered)
 }
 
-static int colred_splits(int rows, int strips) {
-  constexpr int waves = 2;  // target blocks = 2 x SMs (4 and 8 measured slower, profiles/r01d_colred_ab.txt)
-  int s = 1;
-  while (s < CR_MAX_SPLIT && strips * s < waves * num_sms() && rows / (2 * s) >= 64) s *= 2;
-  return s;
+// Splits so that the grid is about one wave at the kernel's smem occupancy (2 / 3 blocks per SM),
+// each split at least 32 rows.
+static int colred_splits(bool ln, int rows, int strips) {
+  const int per_sm = ln ? 2 : 3;  // 64 KB ring + the cross-lane buffer (16.6 / 8.3 KB) per block
+  const int target = per_sm * num_sms();
+  int s = target / strips;  // never more blocks than one wave: a second, short wave doubles the time
+  if (s > CR_MAX_SPLIT) s = CR_MAX_SPLIT;
+  while (s > 1 && rows / s < 32) --s;
+  return s < 1 ? 1 : s;
 }
 
 // ----------------------------------------------------------------------------
@@ -694,6 +769,12 @@ int kernels_preload() {
     cudaError_t e = cudaFuncGetAttributes(&fa, f);
     if (e != cudaSuccess) return set_cuda_error(e, "kernels preload");
   }
+  // column reductions: shared-memory ring beyond the 48 KB default
+  cudaError_t e = cudaFuncSetAttribute(colred_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       colred_smem<true>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(colred_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, colred_smem<false>());
+  if (e != cudaSuccess) return set_cuda_error(e, "colred smem attribute");
   return ZPP_OK;
 }
 
@@ -731,16 +812,17 @@ static int colred_launch(bool ln, const void* dy, long long ld, const void* x, c
                          float* out0, float* out1, float* ws, int rows, int cols, int accumulate, cudaStream_t st) {
   const int strips = (cols + CR_COLS - 1) / CR_COLS;
   const int cols_pad = strips * CR_COLS;
-  const int splits = colred_splits(rows, strips);
+  const int splits = colred_splits(ln, rows, strips);
   float* part = ws;
   unsigned* tickets = reinterpret_cast<unsigned*>(ws + (long long)CR_MAX_SPLIT * 2 * cols_pad);
   dim3 grid(strips, splits);
   if (ln)
-    colred_kernel<true><<<grid, 256, 0, st>>>((const bf16*)dy, ld, (const bf16*)x, mean, rstd, out0, out1, part,
-                                              tickets, rows, cols, cols_pad, accumulate);
+    colred_kernel<true><<<grid, 256, colred_smem<true>(), st>>>((const bf16*)dy, ld, (const bf16*)x, mean, rstd, out0,
+                                                                out1, part, tickets, rows, cols, cols_pad, accumulate);
   else
-    colred_kernel<false><<<grid, 256, 0, st>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr, out0, nullptr, part,
-                                               tickets, rows, cols, cols_pad, accumulate);
+    colred_kernel<false><<<grid, 256, colred_smem<false>(), st>>>((const bf16*)dy, ld, nullptr, nullptr, nullptr,
+                                                                  out0, nullptr, part, tickets, rows, cols, cols_pad,
+                                                                  accumulate);
   return check_launch("colred");
 }
 

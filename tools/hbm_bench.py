@@ -3,7 +3,10 @@ algorithmic bytes vs MEASURED_PEAKS.json hbm_gbs.  CUDA events, median of 20 aft
 import json, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2402_03791_b200.engine import ops
+from paper_2402_03791_b200.engine import lib, ops
+
+if os.environ.get("ZPP_LIB_AB"):  # A/B against another build of the library (tools only)
+    lib.LIB_PATH = os.environ["ZPP_LIB_AB"]
 
 T, h = (int(x) for x in sys.argv[1:3]) if len(sys.argv) > 2 else (4096, 4096)
 dev = "cuda"

@@ -13,6 +13,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 import torch  # noqa: E402
 
+from paper_2402_03791_b200.engine import lib  # noqa: E402
+
+if os.environ.get("ZPP_LIB_AB"):  # A/B against another build of the library (tools only)
+    lib.LIB_PATH = os.environ["ZPP_LIB_AB"]
 from paper_2402_03791_b200 import ModelSpec, ParallelConfig, generate, make_placement  # noqa: E402
 from paper_2402_03791_b200.engine import GPTSpec, Runtime  # noqa: E402
 from paper_2402_03791_b200.engine.data import synthetic_tokens  # noqa: E402
