@@ -690,8 +690,11 @@ static SkParams sk_plan(int tiles, int units, int num_k, int tile_m, int bn, cud
   const int full = tiles / units, r = tiles % units;
   // Measured (tools/gemm_trace.py): parking a 128 KB partial ~6 us and summing it back
   // ~7 us per piece -- the read-back is latency-bound at ~32 KB in flight per SM -- so one
-  // extra piece costs ~22 k-blocks (0.34 us each at 256x256 pair tiles).
-  constexpr int OVH_KB = 22;
+  // extra piece costs ~22 k-blocks (0.34 us each at 256x256 pair tiles) standalone.  In the
+  // step (lower clocks, concurrent kernels) it costs more: with 22 the K = 4096 shapes chose a
+  // 2-piece split and ran 1-4% slower than whole tiles, while K >= 12288 gains 5-7%
+  // (tools/gemm_instep.py --no-streamk, profiles/r02/gemm_streamk_ab.txt); 40 keeps the latter only.
+  constexpr int OVH_KB = 40;
   long long best = (long long)(full + 1) * num_k;
   int best_p = 1;
   for (int p = 2; p <= SK_MAX_PIECES; ++p) {

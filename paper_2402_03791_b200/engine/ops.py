@@ -27,15 +27,23 @@ class _Profile:
         self.active, self.launches, self._gemms = True, 0, []
         self.time_gemms = time_gemms
 
-    def stop(self):
-        """-> (total GEMM FLOPs, summed GEMM launch ms, GEMM launches); synchronizes."""
+    def stop(self, by_shape: bool = False):
+        """-> (total GEMM FLOPs, summed GEMM launch ms, GEMM launches); synchronizes.  With
+        ``by_shape`` also {(M, N, K, a_t, b_t, epilogue): [launches, FLOPs, ms]}."""
         torch.cuda.synchronize()
         self.active = False
-        flops = sum(f for f, _, _ in self._gemms)
-        ms = sum(a.elapsed_time(b) for _, a, b in self._gemms)
+        flops = sum(g[0] for g in self._gemms)
+        ms = sum(g[1].elapsed_time(g[2]) for g in self._gemms)
         n = len(self._gemms)
+        shapes: dict = {}
+        if by_shape:
+            for f, a, b, key in self._gemms:
+                row = shapes.setdefault(key, [0, 0.0, 0.0])
+                row[0] += 1
+                row[1] += f
+                row[2] += a.elapsed_time(b)
         self._gemms = []
-        return flops, ms, n
+        return (flops, ms, n, shapes) if by_shape else (flops, ms, n)
 
 
 PROFILE = _Profile()
@@ -82,7 +90,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_t: bool = False
     if timed:
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(ts)
-        PROFILE._gemms.append((2.0 * M * N * K, e0, e1))
+        PROFILE._gemms.append((2.0 * M * N * K, e0, e1, (M, N, K, int(a_t), int(b_t), epilogue)))
     if PROFILE.shapes is not None:
         out_bytes = c.element_size() * (2 if epilogue == EPI_F32_ACC else 1)
         extra = (resid is not None) + (aux is not None)  # residual read; GeLU pre-act write / dGeLU read
