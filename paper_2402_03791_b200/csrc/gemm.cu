@@ -467,6 +467,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tile_coords(tile, num_m, num_n, n_fast, group, mt, nt);
       const int row0 = mt * TILE_M + crank * GEMM_BM + q * 32;
       const int n0 = nt * BN;
+      if (mode == ZPP_EPI_BF16_DGELU && row0 + lane < M) {
+        // the dGeLU pre-activation this thread's row will read, into L2 while the MMAs run: read
+        // at the point of use it costs an HBM latency per 64-column chunk (FC2 dgrad 121.6 ->
+        // 119.0 ms/step in-step, profiles/r02/gemm_streamk_ab.txt; a residual prefetch gained nothing)
+        const char* a = reinterpret_cast<const char*>(ep.aux + (long long)(row0 + lane) * ep.ldaux + n0);
+        for (int o = 0; o < min(BN, N - n0) * 2; o += 128) prefetch_l2(a + o);
+      }
       if (!own_in_ws) {
         mbar_wait(tfull_bar(acc), acc_phase);
         tc_fence_after();
