@@ -6,8 +6,9 @@ from paper_2402_03791_b200.engine import ops
 ops.preload()
 bf = lambda *s: (torch.randn(*s, device='cuda') * 0.05).to(torch.bfloat16)  # noqa: E731
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device='cuda')
-for name, M, N, K in [("qkv", 12288, 4096, 2048), ("proj", 4096, 4096, 2048), ("fc1", 16384, 4096, 2048),
-                      ("fc2", 4096, 16384, 2048)]:
+K_TOK = int(sys.argv[1]) if len(sys.argv) > 1 else 4096  # tokens per micro-batch (b = 2: 4096)
+for name, M, N, K in [("qkv", 12288, 4096, K_TOK), ("proj", 4096, 4096, K_TOK), ("fc1", 16384, 4096, K_TOK),
+                      ("fc2", 4096, 16384, K_TOK)]:
     A, B = bf(K, M), bf(K, N)
     out = []
     for ep, dt in ((ops.EPI_F32_ACC, torch.float32), (ops.EPI_F32, torch.float32), (ops.EPI_BF16, torch.bfloat16)):
