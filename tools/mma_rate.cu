@@ -266,9 +266,11 @@ int main() {
   run<1, 128, 0, false, true>("cta1 N128 SS K/MN");
   run<1, 128, 0, false, true, true>("cta1 N128 TS K/MN");
   run<1, 64, 0, false, false, true>("cta1 N64 TS K/K");
+  run<1, 32, 0, false, false, true>("cta1 N32 TS K/K");
   run<1, 256, 0, false, true, true>("cta1 N256 TS K/MN");
   run_w<64, false>("warp N64 SS");
   run_w<64, true>("warp N64 TS");
+  run_w<32, true>("warp N32 TS");
   run_w<32, false>("warp N32 SS");
   run_w<128, false>("warp N128 SS");
   run_mix<0>();
