@@ -87,7 +87,7 @@ __device__ __forceinline__ void warp_arrive(uint32_t bar) {
 // one thread can then TMA-store the whole tile: each warp writing 32 different rows straight
 // to global memory cost ~4k cycles of uncoalesced stores per tile (measured, dK/dV epilogue).
 template <int W>
-__device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int c0, uint32_t tile, float mul = 1.f) {
+__device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int c0, uint32_t tile) {
   uint32_t v[32];
   if constexpr (W == 32) {
     tmem_ld32(tacc + lo + c0, v);
@@ -100,10 +100,10 @@ __device__ __forceinline__ void stage_acc(uint32_t tacc, uint32_t lo, int r, int
     const int col = c0 + k;  // multiple of 8: one 16-byte chunk
     const uint32_t atom = tile + (col >> 6) * (128 * 128), chunk = (col & 63) >> 3;
     st_shared_v4(atom + r * 128 + ((chunk ^ (r & 7)) << 4),
-                 pack_bf16(__uint_as_float(v[k]) * mul, __uint_as_float(v[k + 1]) * mul),
-                 pack_bf16(__uint_as_float(v[k + 2]) * mul, __uint_as_float(v[k + 3]) * mul),
-                 pack_bf16(__uint_as_float(v[k + 4]) * mul, __uint_as_float(v[k + 5]) * mul),
-                 pack_bf16(__uint_as_float(v[k + 6]) * mul, __uint_as_float(v[k + 7]) * mul));
+                 pack_bf16(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                 pack_bf16(__uint_as_float(v[k + 2]), __uint_as_float(v[k + 3])),
+                 pack_bf16(__uint_as_float(v[k + 4]), __uint_as_float(v[k + 5])),
+                 pack_bf16(__uint_as_float(v[k + 6]), __uint_as_float(v[k + 7])));
   }
 }
 
@@ -475,36 +475,36 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// dK / dV, persistent: one CTA per SM walks the (128-key block, head) items heaviest first in
-// snake order.  Per 32-query tile g (numbered across the CTA's items):
-//   S^T = K Q^T, dP^T = V dO^T   TS MMAs (A = K / V from TMEM, M = 128 keys, N = 32 queries)
-//                                into TMEM buffer g&1 (S^T and dP^T double-buffered)
-//   row warps: P^T = exp2(S^T - lse2), dS^T = P^T (dP^T - delta) -> bf16, written back in place
-//              over S^T / dP^T (no shared-memory round trip)
-//   dV += P^T dO, dK += dS^T Q   TS MMAs (A = P^T / dS^T from TMEM, B = dO / Q from smem)
-// S / dP(g+2) reuse buffer g&1 and are issued after dV / dK(g): one CTA's MMAs execute in
-// issue order.  32-query tiles are what lets K, V, dK, dV and two S^T / dP^T buffers share the
-// 512 TMEM columns at d = 128 (warp-issued N = 32 TS MMAs run at full rate, tools/mma_rate.cu);
-// with 64-query tiles the single S^T buffer serialised the row warps and the tensor core
-// (profiles/r02/attn_dkdv_pair_ab.txt).
-// warp 0: TMA (K, V per item; Q_t / dO_t + lse2_t / delta_t ring); warp 1: MMA issuer; warp 2:
-// TMEM owner; warps 4..19: row warps, thread = key row (TMEM lane), warp (quarter q, part) takes
-// queries [8 part, 8 part + 8) of each tile; warps 20..23: epilogue (dK / dV -> smem -> TMA).
-// TMEM: dV [0,D) dK [D,2D) K [2D,2D+D/2) V [2D+D/2,3D) S^T [3D,3D+64) (2 x 32) dP^T [3D+64,3D+128).
+// dK / dV, persistent: one CTA per SM walks the (128-key block, head) items heaviest first
+// (item = blockIdx.x + k * gridDim.x), so the next item's K / V load, their copy into TMEM and
+// its first S^T / dP^T MMAs overlap the previous item's last tiles and its dK / dV epilogue
+// (a CTA per item paid ~6k cycles of prologue + ~3k of epilogue on ~25k of tiles).
+// warp 0: TMA (K, V per item; Q_t / dO_t + lse2_t / delta_t through a ring of 3, continuing
+// across items); warp 1: MMA issuer; warp 2: TMEM owner; warps 4..19: row warps, thread = key
+// row (TMEM lane), warp (quarter q, part) takes queries [16 part, 16 part + 16) of each
+// 64-query tile; warps 20..23: epilogue (dK / dV TMEM -> swizzled smem -> TMA store).
+// K and V live in TMEM (A operands of S^T / dP^T: TS-mode MMAs run at the tensor core's rate
+// for N = 64; the SS form re-reads the 128-row A from smem).  S^T / dP^T are single-buffered
+// but released as soon as the row warps have loaded them; P^T and dS^T go to smem (A operands
+// of dV += P^T dO and dK += dS^T Q, N = d: full rate from smem).  The K / V smem tiles double
+// as the epilogue staging area once K / V of the next item sit in TMEM.
+// TMEM: dV [0,D) dK [D,2D) K [2D,2D+D/2) V [2D+D/2,3D) S^T [3D,3D+64) dP^T [3D+64,3D+128).
 template <int D>
 struct BwdDkdvCfg {
-  static constexpr int TQ = 32;            // queries per tile
   static constexpr int KATOM = 128 * 128;  // [128 rows][64 bf16]
   static constexpr int KTILE = (D / 64) * KATOM;
-  static constexpr int QATOM = TQ * 128;   // [32 rows][64 bf16]
+  static constexpr int QATOM = 64 * 128;   // [64 rows][64 bf16]
   static constexpr int QTILE = (D / 64) * QATOM;
-  static constexpr int QST = 4;
+  static constexpr int QST = 3;
+  static constexpr int PT_BYTES = 128 * 128;  // P^T or dS^T: [128 keys][64 queries] bf16
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + KTILE;
   static constexpr int Q_OFF = V_OFF + KTILE;
   static constexpr int DO_OFF = Q_OFF + QST * QTILE;
-  static constexpr int L_OFF = DO_OFF + QST * QTILE;  // per stage: lse2 [32] | delta [32]
-  static constexpr int BAR_OFF = L_OFF + QST * 256;
+  static constexpr int PT_OFF = DO_OFF + QST * QTILE;
+  static constexpr int DS_OFF = PT_OFF + PT_BYTES;
+  static constexpr int L_OFF = DS_OFF + PT_BYTES;  // per stage: lse2 [64] | delta [64]
+  static constexpr int BAR_OFF = L_OFF + QST * 512;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int THREADS = 768;
   static_assert(SMEM <= 232448, "smem budget");
@@ -517,58 +517,27 @@ __global__ void __launch_bounds__(768, 1)
                          const float* __restrict__ lse2, const float* __restrict__ delta, int T, int H, int BH,
                          float scale) {
   using C = BwdDkdvCfg<D>;
-  constexpr int NA = D / 64, TQ = C::TQ;
+  constexpr int NA = D / 64;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t bars = base + C::BAR_OFF;
   const uint32_t kv_full = bars, qd_full0 = bars + 8, qd_empty0 = qd_full0 + 8 * C::QST;
-  const uint32_t kv_tmem = qd_empty0 + 8 * C::QST, sp_full0 = kv_tmem + 8, ds_full0 = sp_full0 + 16;
-  const uint32_t mm_done = ds_full0 + 16, acc_free = mm_done + 8, kv_empty = acc_free + 8;
-  static_assert(8 * (2 * C::QST + 9) <= 240, "barrier area");
+  const uint32_t kv_tmem = qd_empty0 + 8 * C::QST, sp_full = kv_tmem + 8, sp_free = sp_full + 8;
+  const uint32_t ds_full = sp_free + 8, ds_free = ds_full + 8, mm_done = ds_free + 8;
+  const uint32_t acc_free = mm_done + 8, kv_empty = acc_free + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::BAR_OFF + 240);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nitems = (T / 128) * BH;
-  const int G = gridDim.x, cta = blockIdx.x;
   if (threadIdx.x == 128) ZTRACE(1, 0, 63);
-  // Cursor over this CTA's tiles in processing order (items in snake order, TQ-query tiles).
-  struct Cur {
-    int k, j, w, it, nq, g, k0, bh;
-  };
-  auto first_item = [&](Cur& c, int k) {
-    for (; k * G < nitems; ++k) {
-      const int w = snake_item(k, G, cta);
-      if (w < nitems) {
-        c.k = k;
-        c.w = w;
-        c.bh = w % BH;
-        const int kblk = w / BH;
-        c.k0 = kblk * 128;
-        c.nq = (128 / TQ) * (T / 128 - kblk);
-        c.it = 0;
-        return;
-      }
-    }
-    c.k = k;
-    c.w = -1;
-  };
-  auto start = [&](Cur& c) {
-    c.j = 0;
-    c.g = 0;
-    first_item(c, 0);
-  };
-  auto advance = [&](Cur& c) {
-    ++c.g;
-    if (++c.it < c.nq) return;
-    ++c.j;
-    first_item(c, c.k + 1);
-  };
-  auto next_item = [&](Cur& c) {  // skip to the next item (warps that work per item)
-    c.g += c.nq - c.it;
-    ++c.j;
-    first_item(c, c.k + 1);
+  // item w -> (key block, head); item 0.. have the most query tiles
+  auto decode = [&](int w, int& bh, int& k0, int& nq) {
+    bh = w % BH;
+    const int kblk = w / BH;
+    k0 = kblk * 128;
+    nq = 2 * (T / 128 - kblk);
   };
 
   if (threadIdx.x == 0) {
@@ -582,10 +551,10 @@ __global__ void __launch_bounds__(768, 1)
       mbar_init(qd_empty0 + 8 * s, 1);
     }
     mbar_init(kv_tmem, 16);  // one arrival per row warp
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(sp_full0 + 8 * s, 1);
-      mbar_init(ds_full0 + 8 * s, 16);
-    }
+    mbar_init(sp_full, 1);
+    mbar_init(sp_free, 16);
+    mbar_init(ds_full, 16);
+    mbar_init(ds_free, 1);
     mbar_init(mm_done, 1);
     mbar_init(acc_free, 4);  // one arrival per epilogue warp
     mbar_init(kv_empty, 1);
@@ -601,103 +570,120 @@ __global__ void __launch_bounds__(768, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      Cur c;
-      start(c);
-      for (; c.w >= 0; advance(c)) {
-        const int b = c.bh / H, h = c.bh % H, row_base = b * T;
-        if (c.it == 0) {  // K / V of item j (smem free once K / V(j-1) sit in TMEM and, from j == 2,
-                          // once the epilogue of item j-2, staged in the same smem, has been stored)
-          if (c.j == 1) mbar_wait(kv_tmem, 0);
-          if (c.j >= 2) mbar_wait(kv_empty, (c.j - 2) & 1);
-          mbar_arrive_expect_tx(kv_full, 2 * C::KTILE);
-          for (int a = 0; a < NA; ++a) {
-            tma_load_2d(base + C::K_OFF + a * C::KATOM, &tm_kv, kv_full, H * D + h * D + 64 * a, row_base + c.k0);
-            tma_load_2d(base + C::V_OFF + a * C::KATOM, &tm_kv, kv_full, 2 * H * D + h * D + 64 * a,
-                        row_base + c.k0);
-          }
-        }
-        const int st = c.g % C::QST, q0 = c.k0 + c.it * TQ;
-        mbar_wait(qd_empty0 + 8 * st, ((c.g / C::QST) & 1) ^ 1);
-        const uint32_t fb = qd_full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, 2 * C::QTILE + 256);
+      int g = 0;  // running tile index of this CTA (ring stage / parity)
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, k0, nq;
+        decode(w, bh, k0, nq);
+        const int b = bh / H, h = bh % H, row_base = b * T;
+        // K / V smem is free once K / V(j-1) sit in TMEM (j == 1) and, from j == 2 on, once the
+        // epilogue of item j-2 (staged in the same smem) has been stored
+        if (j == 1) mbar_wait(kv_tmem, 0);
+        if (j >= 2) mbar_wait(kv_empty, (j - 2) & 1);
+        mbar_arrive_expect_tx(kv_full, 2 * C::KTILE);
         for (int a = 0; a < NA; ++a) {
-          tma_load_2d(base + C::Q_OFF + st * C::QTILE + a * C::QATOM, &tm_q, fb, h * D + 64 * a, row_base + q0);
-          tma_load_2d(base + C::DO_OFF + st * C::QTILE + a * C::QATOM, &tm_do, fb, h * D + 64 * a, row_base + q0);
+          tma_load_2d(base + C::K_OFF + a * C::KATOM, &tm_kv, kv_full, H * D + h * D + 64 * a, row_base + k0);
+          tma_load_2d(base + C::V_OFF + a * C::KATOM, &tm_kv, kv_full, 2 * H * D + h * D + 64 * a, row_base + k0);
         }
-        if (c.g == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // delta / lse2 of the dQ kernel
-        bulk_load_1d(base + C::L_OFF + st * 256, lse2 + (long long)c.bh * T + q0, 4 * TQ, fb);
-        bulk_load_1d(base + C::L_OFF + st * 256 + 128, delta + (long long)c.bh * T + q0, 4 * TQ, fb);
+        for (int it = 0; it < nq; ++it, ++g) {
+          const int st = g % C::QST;
+          const int q0 = k0 + it * 64;
+          mbar_wait(qd_empty0 + 8 * st, ((g / C::QST) & 1) ^ 1);
+          const uint32_t fb = qd_full0 + 8 * st;
+          mbar_arrive_expect_tx(fb, 2 * C::QTILE + 512);
+          for (int a = 0; a < NA; ++a) {
+            tma_load_2d(base + C::Q_OFF + st * C::QTILE + a * C::QATOM, &tm_q, fb, h * D + 64 * a, row_base + q0);
+            tma_load_2d(base + C::DO_OFF + st * C::QTILE + a * C::QATOM, &tm_do, fb, h * D + 64 * a,
+                        row_base + q0);
+          }
+          if (g == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // delta / lse2 of the dQ kernel
+          bulk_load_1d(base + C::L_OFF + st * 512, lse2 + (long long)bh * T + q0, 256, fb);
+          bulk_load_1d(base + C::L_OFF + st * 512 + 256, delta + (long long)bh * T + q0, 256, fb);
+        }
       }
     }
     __syncwarp();
-  } else if (warp == 1) {  // MMA issuer (whole warp: uniform descriptors, elect.sync issues)
-    constexpr uint32_t id_sp = make_idesc_bf16(128, TQ, false, false);  // S^T, dP^T: N = 32 queries
-    constexpr uint32_t id_kv = make_idesc_bf16(128, D, false, true);    // dV, dK: B N-major (N = d)
-    auto issue_sp = [&](const Cur& c) {  // S^T / dP^T of tile c.g into TMEM buffer c.g & 1
-      const int st = c.g % C::QST, sb = c.g & 1;
-      if (c.it == 0) {
-        mbar_wait(kv_tmem, c.j & 1);  // K, V(j) copied into TMEM
+  } else if (warp == 1) {
+    {  // whole warp: uniform descriptors, elect.sync issues
+      constexpr uint32_t id_sp = make_idesc_bf16(128, 64, false, false);  // S^T, dP^T: N = 64 queries
+      constexpr uint32_t id_kv = make_idesc_bf16(128, D, false, true);    // dV, dK: B N-major (N = d)
+      auto issue_sp = [&](int g) {  // S^T = K Q^T, dP^T = V dO^T of running tile g (A = K / V from TMEM)
+        const int st = g % C::QST;
+        mbar_wait(qd_full0 + 8 * st, (g / C::QST) & 1);
         tc_fence_after();
-      }
-      mbar_wait(qd_full0 + 8 * st, (c.g / C::QST) & 1);
-      tc_fence_after();
-      const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+        const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk)
-        mma_bf16_ts_w(T_S + sb * TQ, T_K + kk * 8, make_sdesc(qs + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024),
-                      id_sp, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_ts_w(T_S, T_K + kk * 8, make_sdesc(qs + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024), id_sp,
+                        kk > 0 ? 1u : 0u);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk)
-        mma_bf16_ts_w(T_DP + sb * TQ, T_V + kk * 8, make_sdesc(dos + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024),
-                      id_sp, kk > 0 ? 1u : 0u);
-      mma_commit_w(sp_full0 + 8 * sb);
-    };
-    Cur sp, mm;
-    start(sp);
-    start(mm);
-    for (int i = 0; i < 2 && sp.w >= 0; ++i, advance(sp)) issue_sp(sp);
-    for (; mm.w >= 0; advance(mm)) {
-      const int st = mm.g % C::QST, sb = mm.g & 1;
-      if (mm.j < 8) ZTRACE(1, 0, mm.it);
-      mbar_wait(ds_full0 + 8 * sb, (mm.g >> 1) & 1);
-      if (mm.j < 8) ZTRACE(1, 1, mm.it);
-      tc_fence_after();
-      if (mm.it == 0 && mm.j > 0) {
-        mbar_wait(acc_free, (mm.j - 1) & 1);  // the epilogue has read dK / dV of item j-1
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_ts_w(T_DP, T_V + kk * 8, make_sdesc(dos + (kk >> 2) * C::QATOM + (kk & 3) * 32, 16, 1024),
+                        id_sp, kk > 0 ? 1u : 0u);
+        mma_commit_w(sp_full);
+      };
+      int g = 0;
+      for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+        int bh, k0, nq;
+        decode(w, bh, k0, nq);
+        mbar_wait(kv_tmem, j & 1);  // K, V(j) copied into TMEM; S^T / dP^T of item j-1 loaded
         tc_fence_after();
-      }
-      const uint32_t acc0 = mm.it > 0 ? 1u : 0u;
-      const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+        issue_sp(g);
+        for (int it = 0; it < nq; ++it, ++g) {
+          const int st = g % C::QST;
+          const uint32_t qs = base + C::Q_OFF + st * C::QTILE, dos = base + C::DO_OFF + st * C::QTILE;
+          if (it + 1 < nq) {
+            mbar_wait(sp_free, g & 1);  // the row warps have loaded S^T(g), dP^T(g)
+            tc_fence_after();
+            issue_sp(g + 1);
+          }
+          if (j < 8) ZTRACE(1, 0, it);
+          mbar_wait(ds_full, g & 1);
+          if (j < 8) ZTRACE(1, 1, it);
+          tc_fence_after();
+          if (it == 0 && j > 0) {
+            mbar_wait(acc_free, (j - 1) & 1);  // the epilogue has read dK / dV of item j-1
+            tc_fence_after();
+          }
+          const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
-      for (int kk = 0; kk < TQ / 16; ++kk)  // dV += P^T dO: A = P^T (bf16 in TMEM, 8 columns per K16)
-        mma_bf16_ts_w(T_DV, T_S + sb * TQ + kk * 8, make_sdesc(dos + kk * 2048, C::QATOM, 1024), id_kv,
-                      (acc0 | kk) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO: A = P^T (smem K-major), B = dO (N-major)
+            mma_bf16_w(T_DV, make_sdesc(base + C::PT_OFF + kk * 32, 16, 1024),
+                       make_sdesc(dos + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
 #pragma unroll
-      for (int kk = 0; kk < TQ / 16; ++kk)  // dK += dS^T Q (dK / scale: the epilogue applies the scale)
-        mma_bf16_ts_w(T_DK, T_DP + sb * TQ + kk * 8, make_sdesc(qs + kk * 2048, C::QATOM, 1024), id_kv,
-                      (acc0 | kk) ? 1u : 0u);
-      mma_commit_w(qd_empty0 + 8 * st);
-      if (mm.it == mm.nq - 1) mma_commit_w(mm_done);
-      if (mm.j < 8) ZTRACE(1, 2, mm.it);
-      if (sp.w >= 0) {  // S / dP(g+2): same TMEM buffer, after dV / dK(g) in the tensor pipe
-        issue_sp(sp);
-        advance(sp);
+          for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q: A = dS^T (smem K-major), B = Q (N-major)
+            mma_bf16_w(T_DK, make_sdesc(base + C::DS_OFF + kk * 32, 16, 1024),
+                       make_sdesc(qs + kk * 2048, C::QATOM, 1024), id_kv, (acc0 | kk) ? 1u : 0u);
+          mma_commit_w(ds_free);
+          mma_commit_w(qd_empty0 + 8 * st);
+          if (j < 8) ZTRACE(1, 2, it);
+        }
+        mma_commit_w(mm_done);
       }
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 20) {  // row warps
+  } else if (warp >= 4 && warp < 20) {
     const int q = warp & 3;
     const int part = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // key row == TMEM lane
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
     const float sl2 = scale * kLog2e;
-    Cur c;
-    start(c);
-    for (; c.w >= 0; advance(c)) {
-      if (c.it == 0) {  // K and V rows of item j -> TMEM (key row r, quarter `part` of the D columns)
-        constexpr int CH = D / 32;
+    int g = 0;
+    for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+      int bh, k0, nq;
+      decode(w, bh, k0, nq);
+      {  // K and V rows of item j -> TMEM (key row r, quarter `part` of the D columns)
+        constexpr int CH = D / 32;  // 16-byte chunks per quarter row
         uint32_t kv[4 * CH], vv[4 * CH];
-        mbar_wait(kv_full, c.j & 1);
+        mbar_wait(kv_full, j & 1);
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
           const int cg = part * CH + i;
@@ -717,84 +703,103 @@ __global__ void __launch_bounds__(768, 1)
         tc_fence_before();
         warp_arrive(kv_tmem);
       }
-      const int sb = c.g & 1;
-      const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (c.g % C::QST) * 256) + part * 8;
-      if (threadIdx.x == 128 && c.j < 8) ZTRACE(1, 4, c.it);
-      mbar_wait(sp_full0 + 8 * sb, (c.g >> 1) & 1);
-      if (threadIdx.x == 128 && c.j < 8) ZTRACE(1, 5, c.it);
-      tc_fence_after();
-      uint32_t sv[8], pv[8];
-      const uint32_t ts = T_S + sb * TQ + lo, tp = T_DP + sb * TQ + lo;
-      tmem_ld8(ts + part * 8, sv);
-      tmem_ld8(tp + part * 8, pv);
-      tmem_wait_ld();
-      float p[8];
+      for (int it = 0; it < nq; ++it, ++g) {
+        const float* L = reinterpret_cast<const float*>(gbase + C::L_OFF + (g % C::QST) * 512) + part * 16;
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 4, it);
+        mbar_wait(sp_full, g & 1);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 5, it);
+        tc_fence_after();
+#ifdef ZPP_TRACE_NOSM  // debug experiment: MMA pipeline alone (row warps only hand over)
+        tc_fence_before();
+        warp_arrive(sp_free);
+        if (g >= 1) mbar_wait(ds_free, (g - 1) & 1);
+        warp_arrive(ds_full);
+        continue;
+#endif
+        uint32_t sv[16], pv[16];
+        tmem_ld16(T_S + lo + part * 16, sv);
+        tmem_ld16(T_DP + lo + part * 16, pv);
+        tmem_wait_ld();
+        tc_fence_before();
+        warp_arrive(sp_free);  // S^T / dP^T of the next tile may now overwrite the buffers
+        float p[16], ds[16];
 #pragma unroll
-      for (int jj = 0; jj < 8; jj += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(L + jj);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        for (int jj = 0; jj < 16; jj += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(L + jj);
+          const float4 d4 = *reinterpret_cast<const float4*>(L + 64 + jj);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) p[jj + u] = fast_exp2(fmaf(__uint_as_float(sv[jj + u]), sl2, -lv[u]));
+          for (int u = 0; u < 4; ++u) {
+            p[jj + u] = fast_exp2(fmaf(__uint_as_float(sv[jj + u]), sl2, -lv[u]));
+            ds[jj + u] = dv[u] * scale;
+          }
+        }
+        if (it < 2) {  // tiles on the diagonal: key after query
+          const int qk = it * 64 + part * 16 - r;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (qk + jj < 0) p[jj] = 0.f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) ds[jj] = p[jj] * fmaf(__uint_as_float(pv[jj]), scale, -ds[jj]);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 6, it);
+        if (g >= 1) mbar_wait(ds_free, (g - 1) & 1);  // dV / dK of the previous tile done reading P^T / dS^T
+        const uint32_t rp = base + C::PT_OFF + r * 128, rd = base + C::DS_OFF + r * 128;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int c8 = part * 2 + t;
+          const float* pp = &p[t * 8];
+          const float* sd = &ds[t * 8];
+          const uint32_t sw = (c8 ^ (r & 7)) << 4;
+          st_shared_v4(rp + sw, pack_bf16(pp[0], pp[1]), pack_bf16(pp[2], pp[3]), pack_bf16(pp[4], pp[5]),
+                       pack_bf16(pp[6], pp[7]));
+          st_shared_v4(rd + sw, pack_bf16(sd[0], sd[1]), pack_bf16(sd[2], sd[3]), pack_bf16(sd[4], sd[5]),
+                       pack_bf16(sd[6], sd[7]));
+        }
+        fence_proxy_async();
+        warp_arrive(ds_full);
+        if (threadIdx.x == 128 && j < 8) ZTRACE(1, 7, it);
       }
-      if (c.it < 128 / TQ) {  // tiles on the diagonal: key after query
-        const int qk = c.it * TQ + part * 8 - r;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (qk + jj < 0) p[jj] = 0.f;
-      }
-      uint32_t pk[4], dk[4];
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const float4 d4 = *reinterpret_cast<const float4*>(L + 32 + (jj >> 1) * 4);
-        const float dlt0 = (jj & 1) ? d4.z : d4.x, dlt1 = (jj & 1) ? d4.w : d4.y;
-        const float d0 = p[2 * jj] * (__uint_as_float(pv[2 * jj]) - dlt0);  // dS / scale
-        const float d1 = p[2 * jj + 1] * (__uint_as_float(pv[2 * jj + 1]) - dlt1);
-        pk[jj] = pack_bf16(p[2 * jj], p[2 * jj + 1]);
-        dk[jj] = pack_bf16(d0, d1);
-      }
-      if (threadIdx.x == 128 && c.j < 8) ZTRACE(1, 6, c.it);
-      // P^T / dS^T overwrite columns [4 part, 4 part + 4) of the S^T / dP^T buffer, which the row
-      // warps of parts 0 and 1 read: all 16 row warps finish their loads first
-      named_bar_sync(1, 512);
-      tmem_st4(ts + part * 4, pk);
-      tmem_st4(tp + part * 4, dk);
-      tmem_wait_st();
-      tc_fence_before();
-      warp_arrive(ds_full0 + 8 * sb);
-      if (threadIdx.x == 128 && c.j < 8) ZTRACE(1, 7, c.it);
     }
-  } else if (warp >= 20) {  // epilogue: thread = key row r of quarter q, all D columns
+  } else if (warp >= 20) {
+    // epilogue warps: thread = TMEM lane (key row) r of quarter q, all D columns
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(q * 32) << 16;
-    Cur c;
-    start(c);
-    for (; c.w >= 0; next_item(c)) {
-      const int b = c.bh / H, h = c.bh % H;
-      Cur nx = c;
-      next_item(nx);
-      mbar_wait(mm_done, c.j & 1);
+    for (int k = 0, jn = 0; k * (int)gridDim.x < nitems; ++k) {
+        const int w = snake_item(k, gridDim.x, blockIdx.x);
+        if (w >= nitems) continue;
+        const int j = jn++;  // this CTA's local item index
+      int bh, k0, nq;
+      decode(w, bh, k0, nq);
+      const int b = bh / H, h = bh % H, row_base = b * T;
+      bool more = false;  // does this CTA take another item after this one?
+      for (int k2 = k + 1; k2 * (int)gridDim.x < nitems && !more; ++k2)
+        more = snake_item(k2, gridDim.x, blockIdx.x) < nitems;
+      mbar_wait(mm_done, j & 1);
       // the staging area is the K / V smem: wait until K / V of the next item are in TMEM
-      if (nx.w >= 0) mbar_wait(kv_tmem, (c.j + 1) & 1);
+      if (more) mbar_wait(kv_tmem, (j + 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < D; cc += 32) {
-        stage_acc<32>(T_DK, lo, r, cc, base + C::K_OFF, scale);  // dK = scale * sum (dS / scale)^T Q
-        stage_acc<32>(T_DV, lo, r, cc, base + C::V_OFF);
+      for (int c = 0; c < D; c += 32) {
+        stage_acc<32>(T_DK, lo, r, c, base + C::K_OFF);
+        stage_acc<32>(T_DV, lo, r, c, base + C::V_OFF);
       }
       tc_fence_before();
-      warp_arrive(acc_free);
+      warp_arrive(acc_free);  // dK / dV read: the MMA warp may start the next item's accumulation
       fence_proxy_async();
       named_bar_sync(2, 128);
       if (threadIdx.x == 640) {
         for (int a = 0; a < NA; ++a) {
-          tma_store_2d(&tm_st, base + C::K_OFF + a * C::KATOM, H * D + h * D + 64 * a, b * T + c.k0);
-          tma_store_2d(&tm_st, base + C::V_OFF + a * C::KATOM, 2 * H * D + h * D + 64 * a, b * T + c.k0);
+          tma_store_2d(&tm_st, base + C::K_OFF + a * C::KATOM, H * D + h * D + 64 * a, row_base + k0);
+          tma_store_2d(&tm_st, base + C::V_OFF + a * C::KATOM, 2 * H * D + h * D + 64 * a, row_base + k0);
         }
         bulk_commit();
         bulk_wait_all();
         mbar_arrive(kv_empty);  // staging smem free: the producer may load K / V of item j+2
+        if (j == 0) ZTRACE(1, 5, 63);
       }
+      if (threadIdx.x == 640 && j == 0) ZTRACE(1, 4, 63);
     }
   }
   tc_fence_before();
@@ -867,11 +872,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* out, const float* lse, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUtensorMap m_q32, m_do32;
-  rc = qkv_map(&m_q32, qkv, H, D, 3, BT, BwdDkdvCfg<D>::TQ);
-  if (!rc) rc = qkv_map(&m_do32, dout, H, D, 1, BT, BwdDkdvCfg<D>::TQ);
-  if (rc) return rc;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q32, m_do32, m_st, (const float*)lse2,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_kernel<D>, m_kv128, m_q64, m_do64, m_st, (const float*)lse2,
                                      (const float*)delta, T, H, BH, scale);
   if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_dkdv launch");
   return check_launch("attn_bwd_dkdv");
